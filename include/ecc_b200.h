@@ -1,0 +1,194 @@
+/*
+ * ecc_b200.h -- C ABI of the B200-native Euler-characteristic-curve engine.
+ *
+ * This is the drop-in boundary for the reference's hot path.
+ * The reference (/root/reference/proj/include/ecc) has no C ABI: it is a
+ * header-only C++20 library.  Every entry point below replaces one reference
+ * call (cited as file:line relative to proj/include/ecc/), and the C++
+ * drop-in headers in include/ecc/ re-expose the reference signatures on top
+ * of these functions.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Pointers documented as "device" are CUDA
+ *    device pointers on the context's GPU; "host" pointers may be pageable or
+ *    pinned.  `stream` is a cudaStream_t passed as void* (NULL = the
+ *    context's own stream).
+ *  - Every function returns ECC_OK (0) or a negative status; the message of
+ *    the last failure on the calling thread is available from
+ *    ecc_last_error().  The C++ headers rethrow it as ecc::error with the
+ *    reference's wording (common.hpp:11-14).
+ *  - Axis 0 (w0) is the slowest axis, axis 2 (w2) the contiguous one; a 2D
+ *    image is w2 == 1 (common.hpp:16-31).
+ *  - There is no CPU fallback: if the CUDA library or a GPU is missing the
+ *    calls fail with ECC_ECUDA.
+ */
+#ifndef ECC_B200_H_
+#define ECC_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ECC_B200_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ECC_API __attribute__((visibility("default")))
+#else
+#define ECC_API
+#endif
+
+enum {
+  ECC_OK = 0,
+  ECC_EINVAL = -1,   /* bad argument / invalid plan (streaming.hpp:186-195) */
+  ECC_ECUDA = -2,    /* CUDA runtime or launch failure, or no device */
+  ECC_ENOMEM = -3,   /* device or pinned allocation failed */
+  ECC_ESOURCE = -4,  /* read_rows callback failed (streaming.hpp:250-259) */
+  ECC_EBINMAP = -5,  /* a value does not fit the requested bin map */
+  ECC_ENAN = -6      /* NaN input (value_index.hpp:29-30, image.hpp:45-48) */
+};
+
+/* Element type of the image.  u8 and f32 are the reference's ValueKind
+ * (common.hpp:43); u16 is the extension BASELINE config 3 needs, with the
+ * reference f32 path as its parity target. */
+typedef enum { ECC_U8 = 0, ECC_U16 = 1, ECC_F32 = 2 } ecc_dtype;
+
+typedef struct {
+  uint64_t w0, w1, w2;
+} ecc_dims;
+
+/* Value -> histogram-bin map; replaces ValueIndex (value_index.hpp:23-85).
+ *  ECC_BIN_IDENTITY : u8/u16, bin = value (256 / 65536 bins).
+ *  ECC_BIN_AFFINE   : f32 quantised to a grid, bin = (v - lo) / step, which
+ *                     must be an exact integer in [0, nbins) and map back to
+ *                     v (checked on the device; failure -> ECC_EBINMAP).
+ *  ECC_BIN_SORTED   : general f32: distinct values found by a device radix
+ *                     sort + reduce-by-key (build_index_counts,
+ *                     value_index.hpp:159-197). */
+enum { ECC_BIN_IDENTITY = 0, ECC_BIN_AFFINE = 1, ECC_BIN_SORTED = 2 };
+
+typedef struct {
+  int32_t kind;
+  uint32_t nbins; /* AFFINE only */
+  float lo;       /* AFFINE only */
+  float step;     /* AFFINE only */
+} ecc_binmap;
+
+/* Per-chunk phase times in seconds since the call began (ChunkTiming,
+ * streaming.hpp:83-89).  ingest = read_rows + H2D, kernel = stencil +
+ * histogram on the device, merge = device histogram reduction. */
+typedef struct {
+  uint64_t begin, end;
+  double ingest_begin, ingest_end;
+  double index_begin, index_end;
+  double kernel_begin, kernel_end;
+  double merge_begin, merge_end;
+} ecc_chunk_timing;
+
+typedef struct ecc_ctx ecc_ctx;
+
+/* ------------------------------------------------------------ context */
+ECC_API int ecc_abi_version(void);
+ECC_API const char* ecc_last_error(void);
+/* One context per GPU; it owns a stream, scratch and pinned staging. */
+ECC_API int ecc_ctx_create(int device, ecc_ctx** out);
+ECC_API void ecc_ctx_destroy(ecc_ctx* ctx);
+/* The context's own stream (cudaStream_t). */
+ECC_API void* ecc_ctx_stream(ecc_ctx* ctx);
+/* Number of my kernels launched by this context since creation. */
+ECC_API uint64_t ecc_ctx_launch_count(ecc_ctx* ctx);
+
+/* Number of histogram bins for (dtype, binmap); ECC_BIN_SORTED -> 0. */
+ECC_API int ecc_bin_count(ecc_dtype dtype, const ecc_binmap* bm, uint64_t* nbins);
+
+/* ------------------------------------------------------------ L2: slab kernels
+ * A slab is the reference's PaddedChunk (chunk.hpp:50-127): owned rows
+ * [own0, own1) along axis 0 plus one halo plane on each side when it exists
+ * inside the image; outside the image the collar sentinel applies
+ * (common.hpp:49-66).  `d_planes` holds image planes [plane0,
+ * plane0 + nplanes) contiguously and must cover
+ * [max(own0,1)-1, min(own1+1, w0)). */
+
+/* Stencil + histogram (K1+K2): adds the slab's per-bin change sums to
+ * d_hist[0..nbins) and per-bin voxel counts to d_hist[nbins..2*nbins)
+ * (int64, device).  Replaces accumulate_dense_u8 (kernel.hpp:268-277),
+ * run_chunk_kernel_u8 (streaming.hpp:146-174) and accumulate_chunk
+ * (kernel.hpp:229-239).  Not valid for ECC_BIN_SORTED. */
+ECC_API int ecc_accumulate_slab(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
+                        ecc_dims image, uint64_t plane0, uint64_t nplanes,
+                        uint64_t own0, uint64_t own1, const ecc_binmap* bm,
+                        int64_t* d_hist, void* stream);
+
+/* Per-voxel Euler changes of the owned rows, int8, owned row-major order
+ * (compute_changes, kernel.hpp:244-265 with change_2d/change_3d/
+ * change_row_3d, kernel.hpp:81-188).  d_out: device. */
+ECC_API int ecc_compute_changes(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
+                        ecc_dims image, uint64_t plane0, uint64_t nplanes,
+                        uint64_t own0, uint64_t own1, int8_t* d_out,
+                        void* stream);
+
+/* ------------------------------------------------------------ L3: merge + curve
+ * K3: compacts the occurring bins of a dense histogram (merge_local,
+ * vcec.hpp:35-66) and prefix-sums them (vcec_to_ecc, curve.hpp:28-35).
+ * Outputs are device arrays of capacity nbins; *d_count (device uint64) gets
+ * the number of occurring bins. */
+ECC_API int ecc_finalize(ecc_ctx* ctx, const int64_t* d_hist, uint64_t nbins,
+                 uint32_t* d_bins, int64_t* d_changes, int64_t* d_chi,
+                 uint64_t* d_count, void* stream);
+
+/* ------------------------------------------------------------ L4: whole images
+ * process_image(const Image<T>&, plan) (streaming.hpp:332-338) + the VCEC
+ * result.  `data` is host (where = 0) or device (where = 1).  Outputs are
+ * host arrays: values_out (dtype elements) and changes_out (int64), capacity
+ * `cap`; *n_out = number of occurring values.  The result is independent of
+ * any chunking (acceptance.cpp:203-227), so no plan is taken. */
+ECC_API int ecc_vcec(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
+             ecc_dims dims, const ecc_binmap* bm, void* values_out,
+             int64_t* changes_out, uint64_t cap, uint64_t* n_out);
+
+/* Same, returning the curve (vcec_to_ecc): thresholds + chi. */
+ECC_API int ecc_curve(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
+              ecc_dims dims, const ecc_binmap* bm, void* thresholds_out,
+              int64_t* chi_out, uint64_t cap, uint64_t* n_out);
+
+/* ------------------------------------------------------------ L4: streaming
+ * process_image(ChunkSource<T>&, const ChunkPlan&, ...) (streaming.hpp:
+ * 181-329).  Rows arrive through `read_rows` (ChunkSource::read_rows,
+ * chunk.hpp:131-137), which fills `dst` (pinned host staging) with image
+ * rows [r0, r1) and returns 0, or nonzero with a message in errbuf.
+ * `bounds` holds nchunks+1 ascending row indices (the plan's ranges).
+ * Ingestion of chunk k+1 overlaps the device work of chunk k. */
+typedef int (*ecc_read_rows_fn)(void* user, uint64_t r0, uint64_t r1,
+                                void* dst, char* errbuf, size_t errlen);
+
+ECC_API int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
+                       ecc_dtype dtype, ecc_dims dims, const uint64_t* bounds,
+                       size_t nchunks, const ecc_binmap* bm,
+                       ecc_chunk_timing* timings, void* values_out,
+                       int64_t* changes_out, uint64_t cap, uint64_t* n_out);
+
+/* ------------------------------------------------------------ batched 2D
+ * New entry point (the reference has none): `count` images of
+ * h x w (axis 0 = h), stored back to back.  For each image b, writes the
+ * dense curve chi[b][t] = chi(K_<=t) for every bin t (int32; 256 or 65536
+ * bins) and a presence bitmap presence[b][t/32] (bit t%32 set iff value t
+ * occurs).  data/chi/presence are all device (where = 1) or all host
+ * (where = 0). */
+ECC_API int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
+                uint64_t count, uint64_t h, uint64_t w, int32_t* chi,
+                uint32_t* presence, void* stream);
+
+/* ------------------------------------------------------------ synthetic inputs
+ * Device fill with the reference generator (datagen.hpp:18-27): element i
+ * gets counter_hash(seed, base + i) >> 56 (u8), >> 48 (u16) or
+ * float(H >> 48) * 2^-16 (f32).  Used by the bench and tests. */
+ECC_API int ecc_fill_synthetic(ecc_ctx* ctx, void* d_data, ecc_dtype dtype,
+                       uint64_t n, uint64_t seed, uint64_t base, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ECC_B200_H_ */

@@ -1,0 +1,747 @@
+// capi.cu -- implementation of the C ABI in include/ecc_b200.h.
+//
+// Host orchestration only: argument validation with the reference's error
+// wording, scratch management, the streaming driver (pinned staging, a copy
+// stream and a compute stream), and dispatch to the kernels.  All voxel
+// work happens in the kernels; there is no host compute path.
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
+
+#include "../../include/ecc_b200.h"
+#include "internal.h"
+
+using namespace eccb;
+
+namespace eccb {
+cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, int w,
+                           int32_t* chi, uint32_t* presence, cudaStream_t st);
+cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
+                                   const AffineMap& am, int64_t* ghist,
+                                   uint32_t nbins, uint32_t* flags, int sms,
+                                   cudaStream_t st, bool* handled);
+}  // namespace eccb
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CKR(x)                                                               \
+  do {                                                                       \
+    cudaError_t e_ = (x);                                                    \
+    if (e_ != cudaSuccess)                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? ECC_ENOMEM : ECC_ECUDA,  \
+                  std::string("CUDA error in ") + #x + ": " +                \
+                      cudaGetErrorString(e_));                               \
+  } while (0)
+
+#define CKI(x)                        \
+  do {                                \
+    int rc_ = (x);                    \
+    if (rc_ != ECC_OK) return rc_;    \
+  } while (0)
+
+size_t esize(ecc_dtype t) { return t == ECC_U8 ? 1 : (t == ECC_U16 ? 2 : 4); }
+
+std::string dims_str(const ecc_dims& d) {
+  return std::to_string(d.w0) + "x" + std::to_string(d.w1) + "x" + std::to_string(d.w2);
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return ECC_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ECC_ENOMEM, "device allocation of " + std::to_string(want) +
+                                  " bytes failed: " + cudaGetErrorString(e));
+    }
+    cap = want;
+    return ECC_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct PinBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return ECC_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(ECC_ENOMEM, "pinned allocation of " + std::to_string(bytes) +
+                                  " bytes failed: " + cudaGetErrorString(e));
+    }
+    cap = bytes;
+    return ECC_OK;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct ecc_ctx {
+  int device = 0;
+  int sms = 148;
+  cudaStream_t stream = nullptr;  // compute
+  cudaStream_t copy = nullptr;    // H2D
+  uint64_t launches = 0;
+  DevBuf input, hist, bins, changes, chi, count, flags;
+  DevBuf keys, keys2, ch8, ch8b, sums, tmp;
+  DevBuf slab[2];
+  PinBuf staging[2];
+  PinBuf host_small;
+};
+
+namespace {
+
+int bind(ecc_ctx* ctx) {
+  if (!ctx) return fail(ECC_EINVAL, "null context");
+  CKR(cudaSetDevice(ctx->device));
+  return ECC_OK;
+}
+
+cudaStream_t pick(ecc_ctx* ctx, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+}
+
+int check_dtype(ecc_dtype t) {
+  if (t != ECC_U8 && t != ECC_U16 && t != ECC_F32)
+    return fail(ECC_EINVAL, "unknown dtype " + std::to_string((int)t));
+  return ECC_OK;
+}
+
+int check_dims(const ecc_dims& d) {
+  if (d.w0 < 1 || d.w1 < 1 || d.w2 < 1)
+    return fail(ECC_EINVAL, "dims must be >= 1, got " + dims_str(d));
+  return ECC_OK;
+}
+
+// Resolves (dtype, binmap) to a bin count and an affine map.
+int resolve_bins(ecc_dtype dtype, const ecc_binmap* bm, uint64_t* nbins,
+                 bool* affine, bool* sorted, AffineMap* am) {
+  const int kind = bm ? bm->kind : (dtype == ECC_F32 ? ECC_BIN_SORTED : ECC_BIN_IDENTITY);
+  *affine = false;
+  *sorted = false;
+  if (dtype == ECC_U8 || dtype == ECC_U16) {
+    if (kind != ECC_BIN_IDENTITY)
+      return fail(ECC_EINVAL, "integer images use the identity bin map");
+    *nbins = dtype == ECC_U8 ? 256 : 65536;
+    return ECC_OK;
+  }
+  if (kind == ECC_BIN_SORTED) {
+    *sorted = true;
+    *nbins = 0;
+    return ECC_OK;
+  }
+  if (kind != ECC_BIN_AFFINE)
+    return fail(ECC_EINVAL, "f32 images need an affine or sorted bin map");
+  if (!(bm->step > 0.0f) || bm->nbins < 1 || bm->nbins > (1u << 24) || bm->lo != bm->lo)
+    return fail(ECC_EINVAL, "invalid affine bin map");
+  *affine = true;
+  *nbins = bm->nbins;
+  am->lo = bm->lo;
+  am->step = bm->step;
+  am->inv_step = 1.0 / (double)bm->step;
+  am->nbins = bm->nbins;
+  return ECC_OK;
+}
+
+int check_slab(ecc_dims d, uint64_t plane0, uint64_t nplanes, uint64_t own0,
+               uint64_t own1) {
+  CKI(check_dims(d));
+  if (!(own0 < own1) || own1 > d.w0)
+    return fail(ECC_EINVAL, "invalid chunk range [" + std::to_string(own0) + ", " +
+                                std::to_string(own1) + ") for dims " + dims_str(d));
+  const uint64_t need0 = own0 == 0 ? 0 : own0 - 1;
+  const uint64_t need1 = std::min<uint64_t>(own1 + 1, d.w0);
+  if (plane0 > need0 || plane0 + nplanes < need1)
+    return fail(ECC_EINVAL, "slab buffer planes [" + std::to_string(plane0) + ", " +
+                                std::to_string(plane0 + nplanes) +
+                                ") do not cover the halo range [" + std::to_string(need0) +
+                                ", " + std::to_string(need1) + ")");
+  return ECC_OK;
+}
+
+Slab make_slab(const void* base, ecc_dims d, uint64_t plane0, uint64_t nplanes,
+               uint64_t own0, uint64_t own1) {
+  Slab s;
+  s.base = base;
+  s.plane0 = (int64_t)plane0;
+  s.nplanes = (int64_t)nplanes;
+  s.w0 = (int64_t)d.w0;
+  s.w1 = (int64_t)d.w1;
+  s.w2 = (int64_t)d.w2;
+  s.own0 = (int64_t)own0;
+  s.own1 = (int64_t)own1;
+  return s;
+}
+
+int read_flags(ecc_ctx* ctx, cudaStream_t st) {
+  uint32_t f = 0;
+  CKR(cudaMemcpyAsync(&f, ctx->flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  if (f & kFlagNaN) return fail(ECC_ENAN, "cannot build a value index: NaN input");
+  if (f & kFlagBinmap)
+    return fail(ECC_EBINMAP, "a value does not lie on the affine bin grid");
+  return ECC_OK;
+}
+
+// Accumulate one slab into ctx->hist (already zeroed), dispatching to the
+// specialised kernels when they cover the shape.
+int accumulate(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine,
+               const AffineMap& am, uint32_t nbins, int64_t* hist, cudaStream_t st) {
+  bool handled = false;
+  CKR(launch_accumulate_fast(s, (int)dtype, affine, am, hist, nbins,
+                             ctx->flags.as<uint32_t>(), ctx->sms, st, &handled));
+  if (!handled)
+    CKR(launch_generic_accumulate(s, (int)dtype, affine, am, hist, nbins,
+                                  ctx->flags.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+// Result of a whole-volume or streamed run, in bin space.
+struct BinResult {
+  std::vector<uint32_t> bins;     // identity / affine
+  std::vector<uint32_t> keys;     // sorted path (order keys)
+  std::vector<int64_t> changes;
+  std::vector<int64_t> chi;
+};
+
+int finalize_to_host(ecc_ctx* ctx, uint32_t nbins, cudaStream_t st, BinResult* out) {
+  CKI(ctx->bins.ensure(nbins * 4ull));
+  CKI(ctx->changes.ensure(nbins * 8ull));
+  CKI(ctx->chi.ensure(nbins * 8ull));
+  CKI(ctx->count.ensure(8));
+  CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, ctx->bins.as<uint32_t>(),
+                      ctx->changes.as<int64_t>(), ctx->chi.as<int64_t>(),
+                      ctx->count.as<uint64_t>(), st));
+  ctx->launches += 1;
+  uint64_t m = 0;
+  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  out->bins.resize(m);
+  out->changes.resize(m);
+  out->chi.resize(m);
+  if (m) {
+    CKR(cudaMemcpyAsync(out->bins.data(), ctx->bins.p, m * 4, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->changes.data(), ctx->changes.p, m * 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->chi.data(), ctx->chi.p, m * 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+  }
+  return ECC_OK;
+}
+
+// General f32 path (build_index_counts, value_index.hpp:159-197, on the
+// device): per-voxel int8 changes + order keys, radix argsort by key,
+// reduce-by-key into (distinct value, summed change).  Appends the slab's
+// (key, sum) runs to `out` (unmerged; caller merges across slabs).
+struct ToI64 {
+  __host__ __device__ int64_t operator()(int8_t v) const { return v; }
+};
+
+int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st,
+                std::vector<uint32_t>* keys_out, std::vector<int64_t>* sums_out) {
+  const uint64_t n64 = (uint64_t)(s.own1 - s.own0) * s.w1 * s.w2;
+  if (n64 > 0x7FFFFFFFull)
+    return fail(ECC_EINVAL, "chunk exceeds 2^31 voxels; use a finer chunk plan");
+  const int n = (int)n64;
+  CKI(ctx->keys.ensure(n64 * 4));
+  CKI(ctx->keys2.ensure(n64 * 4));
+  CKI(ctx->ch8.ensure(n64));
+  CKI(ctx->ch8b.ensure(n64));
+  CKI(ctx->sums.ensure(n64 * 8));
+  CKI(ctx->count.ensure(8));
+  CKR(launch_generic_changes(s, ECC_F32, ctx->ch8.as<int8_t>(), ctx->sms, st));
+  const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
+  CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), ctx->flags.as<uint32_t>(),
+                        ctx->sms, st));
+  ctx->launches += 2;
+  size_t t1 = 0, t2 = 0;
+  CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, ctx->keys.as<uint32_t>(),
+                                      ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
+                                      ctx->ch8b.as<int8_t>(), n, 0, 32, st));
+  auto vals = thrust::make_transform_iterator(ctx->ch8b.as<const int8_t>(), ToI64());
+  CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(),
+                                     ctx->keys.as<uint32_t>(), vals, ctx->sums.as<int64_t>(),
+                                     ctx->count.as<uint64_t>(), cub::Sum(), n, st));
+  CKI(ctx->tmp.ensure(std::max(t1, t2)));
+  t1 = ctx->tmp.cap;
+  CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, ctx->keys.as<uint32_t>(),
+                                      ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
+                                      ctx->ch8b.as<int8_t>(), n, 0, 32, st));
+  t2 = ctx->tmp.cap;
+  CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(),
+                                     ctx->keys.as<uint32_t>(), vals, ctx->sums.as<int64_t>(),
+                                     ctx->count.as<uint64_t>(), cub::Sum(), n, st));
+  ctx->launches += 2;
+  uint64_t m = 0;
+  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  const size_t off = keys_out->size();
+  keys_out->resize(off + m);
+  sums_out->resize(off + m);
+  CKR(cudaMemcpyAsync(keys_out->data() + off, ctx->keys.p, m * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaMemcpyAsync(sums_out->data() + off, ctx->sums.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+// merge_local (vcec.hpp:35-66) of sorted (key, sum) runs from several slabs.
+void merge_runs(const std::vector<uint32_t>& keys, const std::vector<int64_t>& sums,
+                const std::vector<size_t>& starts, BinResult* out) {
+  std::vector<std::pair<uint32_t, int64_t>> all;
+  all.reserve(keys.size());
+  for (size_t i = 0; i < keys.size(); ++i) all.emplace_back(keys[i], sums[i]);
+  if (starts.size() > 2) std::stable_sort(all.begin(), all.end(),
+                                          [](auto& a, auto& b) { return a.first < b.first; });
+  out->keys.clear();
+  out->changes.clear();
+  for (auto& [k, v] : all) {
+    if (!out->keys.empty() && out->keys.back() == k)
+      out->changes.back() += v;
+    else {
+      out->keys.push_back(k);
+      out->changes.push_back(v);
+    }
+  }
+  out->chi.resize(out->changes.size());
+  int64_t acc = 0;
+  for (size_t i = 0; i < out->changes.size(); ++i) out->chi[i] = acc += out->changes[i];
+}
+
+float key_to_float(uint32_t k) {
+  const uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// Writes thresholds (dtype elements) for the result.
+void write_values(ecc_dtype dtype, bool sorted, const AffineMap& am, const BinResult& r,
+                  void* out) {
+  const size_t m = sorted ? r.keys.size() : r.bins.size();
+  for (size_t i = 0; i < m; ++i) {
+    if (dtype == ECC_U8)
+      static_cast<uint8_t*>(out)[i] = (uint8_t)r.bins[i];
+    else if (dtype == ECC_U16)
+      static_cast<uint16_t*>(out)[i] = (uint16_t)r.bins[i];
+    else if (sorted)
+      static_cast<float*>(out)[i] = key_to_float(r.keys[i]);
+    else
+      static_cast<float*>(out)[i] = affine_value(am, r.bins[i]);
+  }
+}
+
+// Whole device-resident volume -> BinResult.
+int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
+               const ecc_binmap* bm, cudaStream_t st, BinResult* res, bool* sorted_out,
+               AffineMap* am_out) {
+  uint64_t nbins = 0;
+  bool affine = false, sorted = false;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  *sorted_out = sorted;
+  *am_out = am;
+  CKI(ctx->flags.ensure(4));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  const Slab s = make_slab(d_data, dims, 0, dims.w0, 0, dims.w0);
+  if (sorted) {
+    std::vector<uint32_t> keys;
+    std::vector<int64_t> sums;
+    CKI(sorted_slab(ctx, s, st, &keys, &sums));
+    CKI(read_flags(ctx, st));
+    merge_runs(keys, sums, {0, keys.size()}, res);
+    return ECC_OK;
+  }
+  CKI(ctx->hist.ensure(2 * nbins * 8));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
+  CKI(finalize_to_host(ctx, (uint32_t)nbins, st, res));
+  CKI(read_flags(ctx, st));
+  return ECC_OK;
+}
+
+int stage_input(ecc_ctx* ctx, const void* data, int where, uint64_t bytes,
+                cudaStream_t st, const void** d_data) {
+  if (where == 1) {
+    *d_data = data;
+    return ECC_OK;
+  }
+  if (where != 0) return fail(ECC_EINVAL, "where must be 0 (host) or 1 (device)");
+  CKI(ctx->input.ensure(bytes));
+  CKR(cudaMemcpyAsync(ctx->input.p, data, bytes, cudaMemcpyHostToDevice, st));
+  *d_data = ctx->input.p;
+  return ECC_OK;
+}
+
+}  // namespace
+
+// ===================================================================== ABI
+extern "C" {
+
+int ecc_abi_version(void) { return ECC_B200_ABI_VERSION; }
+
+const char* ecc_last_error(void) { return g_err.c_str(); }
+
+int ecc_ctx_create(int device, ecc_ctx** out) {
+  if (!out) return fail(ECC_EINVAL, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(ECC_ECUDA, std::string("no CUDA device available: ") +
+                               (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices"));
+  }
+  if (device < 0 || device >= ndev)
+    return fail(ECC_EINVAL, "device " + std::to_string(device) + " out of range");
+  CKR(cudaSetDevice(device));
+  auto* ctx = new ecc_ctx();
+  ctx->device = device;
+  CKR(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+  CKR(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CKR(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+  *out = ctx;
+  return ECC_OK;
+}
+
+void ecc_ctx_destroy(ecc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->copy);
+  for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
+                    &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
+                    &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1]})
+    b->release();
+  ctx->staging[0].release();
+  ctx->staging[1].release();
+  ctx->host_small.release();
+  cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->copy);
+  delete ctx;
+}
+
+void* ecc_ctx_stream(ecc_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+uint64_t ecc_ctx_launch_count(ecc_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int ecc_bin_count(ecc_dtype dtype, const ecc_binmap* bm, uint64_t* nbins) {
+  CKI(check_dtype(dtype));
+  bool a, s;
+  AffineMap am;
+  return resolve_bins(dtype, bm, nbins, &a, &s, &am);
+}
+
+int ecc_accumulate_slab(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
+                        ecc_dims image, uint64_t plane0, uint64_t nplanes,
+                        uint64_t own0, uint64_t own1, const ecc_binmap* bm,
+                        int64_t* d_hist, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_slab(image, plane0, nplanes, own0, own1));
+  if (!d_planes || !d_hist) return fail(ECC_EINVAL, "null device pointer");
+  uint64_t nbins;
+  bool affine, sorted;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  if (sorted) return fail(ECC_EINVAL, "the sorted bin map has no dense histogram");
+  cudaStream_t st = pick(ctx, stream);
+  CKI(ctx->flags.ensure(4));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  const Slab s = make_slab(d_planes, image, plane0, nplanes, own0, own1);
+  CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, d_hist, st));
+  if (affine) CKI(read_flags(ctx, st));
+  return ECC_OK;
+}
+
+int ecc_compute_changes(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
+                        ecc_dims image, uint64_t plane0, uint64_t nplanes,
+                        uint64_t own0, uint64_t own1, int8_t* d_out, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_slab(image, plane0, nplanes, own0, own1));
+  if (!d_planes || !d_out) return fail(ECC_EINVAL, "null device pointer");
+  const Slab s = make_slab(d_planes, image, plane0, nplanes, own0, own1);
+  CKR(launch_generic_changes(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream)));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+int ecc_finalize(ecc_ctx* ctx, const int64_t* d_hist, uint64_t nbins, uint32_t* d_bins,
+                 int64_t* d_changes, int64_t* d_chi, uint64_t* d_count, void* stream) {
+  CKI(bind(ctx));
+  if (!d_hist || !d_bins || !d_changes || !d_chi || !d_count)
+    return fail(ECC_EINVAL, "null device pointer");
+  if (nbins < 1 || nbins > (1u << 24)) return fail(ECC_EINVAL, "bad bin count");
+  CKR(launch_finalize(d_hist, (uint32_t)nbins, d_bins, d_changes, d_chi, d_count,
+                      pick(ctx, stream)));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
+                         ecc_dims dims, const ecc_binmap* bm, void* values_out,
+                         int64_t* series_out, uint64_t cap, uint64_t* n_out, bool want_chi) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_dims(dims));
+  if (!data || !values_out || !series_out || !n_out) return fail(ECC_EINVAL, "null pointer");
+  cudaStream_t st = ctx->stream;
+  const uint64_t bytes = dims.w0 * dims.w1 * dims.w2 * esize(dtype);
+  const void* d_data = nullptr;
+  CKI(stage_input(ctx, data, where, bytes, st, &d_data));
+  BinResult r;
+  bool sorted = false;
+  AffineMap am{};
+  CKI(run_volume(ctx, d_data, dtype, dims, bm, st, &r, &sorted, &am));
+  const size_t m = r.changes.size();
+  *n_out = m;
+  if (m > cap) return fail(ECC_EINVAL, "output capacity " + std::to_string(cap) +
+                                           " is below the " + std::to_string(m) + " values");
+  write_values(dtype, sorted, am, r, values_out);
+  std::memcpy(series_out, want_chi ? r.chi.data() : r.changes.data(), m * 8);
+  return ECC_OK;
+}
+
+int ecc_vcec(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, ecc_dims dims,
+             const ecc_binmap* bm, void* values_out, int64_t* changes_out, uint64_t cap,
+             uint64_t* n_out) {
+  return volume_common(ctx, data, where, dtype, dims, bm, values_out, changes_out, cap,
+                       n_out, false);
+}
+
+int ecc_curve(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, ecc_dims dims,
+              const ecc_binmap* bm, void* thresholds_out, int64_t* chi_out, uint64_t cap,
+              uint64_t* n_out) {
+  return volume_common(ctx, data, where, dtype, dims, bm, thresholds_out, chi_out, cap,
+                       n_out, true);
+}
+
+int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
+                       ecc_dtype dtype, ecc_dims dims, const uint64_t* bounds,
+                       size_t nchunks, const ecc_binmap* bm, ecc_chunk_timing* timings,
+                       void* values_out, int64_t* changes_out, uint64_t cap,
+                       uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  if (dims.w0 < 1) return fail(ECC_EINVAL, "w0 must be >= 1");
+  CKI(check_dims(dims));
+  if (!read_rows || !values_out || !changes_out || !n_out)
+    return fail(ECC_EINVAL, "null pointer");
+  // plan validation, streaming.hpp:186-195
+  if (nchunks == 0 || !bounds) return fail(ECC_EINVAL, "empty chunk plan");
+  if (bounds[0] != 0) return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  for (size_t k = 0; k < nchunks; ++k)
+    if (bounds[k + 1] <= bounds[k])
+      return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  if (bounds[nchunks] != dims.w0)
+    return fail(ECC_EINVAL, "chunk plan covers [0, " + std::to_string(bounds[nchunks]) +
+                                ") but the source has w0 = " + std::to_string(dims.w0));
+  uint64_t nbins = 0;
+  bool affine = false, sorted = false;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+
+  const auto t0 = std::chrono::steady_clock::now();
+  auto since = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const uint64_t row_bytes = dims.w1 * dims.w2 * esize(dtype);
+  uint64_t max_rows = 0;
+  for (size_t k = 0; k < nchunks; ++k)
+    max_rows = std::max<uint64_t>(max_rows, bounds[k + 1] - bounds[k] + 2);
+  max_rows = std::min<uint64_t>(max_rows, dims.w0);
+  const uint64_t buf_bytes = max_rows * row_bytes;
+  for (int b = 0; b < 2; ++b) {
+    CKI(ctx->staging[b].ensure(buf_bytes));
+    CKI(ctx->slab[b].ensure(buf_bytes));
+  }
+  CKI(ctx->flags.ensure(4));
+  cudaStream_t st = ctx->stream, cp = ctx->copy;
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  if (!sorted) {
+    CKI(ctx->hist.ensure(2 * nbins * 8));
+    CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  }
+  cudaEvent_t ev0, h2d_done[2], used[2], kb[2], ke[2];
+  CKR(cudaEventCreate(&ev0));
+  for (int b = 0; b < 2; ++b) {
+    CKR(cudaEventCreate(&h2d_done[b]));
+    CKR(cudaEventCreate(&used[b]));
+    CKR(cudaEventCreate(&kb[b]));
+    CKR(cudaEventCreate(&ke[b]));
+  }
+  CKR(cudaEventRecord(ev0, st));
+  std::vector<uint32_t> skeys;
+  std::vector<int64_t> ssums;
+  std::vector<size_t> starts{0};
+  std::vector<ecc_chunk_timing> tim(nchunks);
+  std::vector<double> h2d_end_host(nchunks, 0);
+  int rc = ECC_OK;
+  bool pending[2] = {false, false};
+  size_t pending_k[2] = {0, 0};
+  auto harvest = [&](int b) -> int {
+    // event timings for the chunk that last used buffer b
+    if (!pending[b]) return ECC_OK;
+    CKR(cudaEventSynchronize(ke[b]));
+    float a = 0, c = 0;
+    CKR(cudaEventElapsedTime(&a, ev0, kb[b]));
+    CKR(cudaEventElapsedTime(&c, ev0, ke[b]));
+    ecc_chunk_timing& t = tim[pending_k[b]];
+    t.kernel_begin = a * 1e-3;
+    t.kernel_end = c * 1e-3;
+    pending[b] = false;
+    return ECC_OK;
+  };
+  for (size_t k = 0; k < nchunks && rc == ECC_OK; ++k) {
+    const int b = (int)(k & 1);
+    const uint64_t own0 = bounds[k], own1 = bounds[k + 1];
+    const uint64_t r0 = own0 == 0 ? 0 : own0 - 1;
+    const uint64_t r1 = std::min<uint64_t>(own1 + 1, dims.w0);
+    // the pinned buffer b was last read by the H2D copy of chunk k-2
+    CKR(cudaEventSynchronize(used[b]));
+    ecc_chunk_timing& t = tim[k];
+    t.begin = own0;
+    t.end = own1;
+    t.ingest_begin = since();
+    char errbuf[512] = {0};
+    const int src = read_rows(user, r0, r1, ctx->staging[b].p, errbuf, sizeof errbuf);
+    if (src != 0) {
+      rc = fail(ECC_ESOURCE, "ingestion of chunk " + std::to_string(k) + " failed: " +
+                                 std::string(errbuf[0] ? errbuf : "read_rows failed"));
+      break;
+    }
+    // the device buffer b was last read by the kernel of chunk k-2
+    CKR(cudaStreamWaitEvent(cp, ke[b], 0));
+    CKR(cudaMemcpyAsync(ctx->slab[b].p, ctx->staging[b].p, (r1 - r0) * row_bytes,
+                        cudaMemcpyHostToDevice, cp));
+    CKR(cudaEventRecord(used[b], cp));
+    CKR(cudaEventRecord(h2d_done[b], cp));
+    t.ingest_end = since();
+    t.index_begin = t.index_end = t.ingest_end;
+    CKI(harvest(b));
+    CKR(cudaStreamWaitEvent(st, h2d_done[b], 0));
+    CKR(cudaEventRecord(kb[b], st));
+    const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
+    t.merge_begin = since();
+    if (sorted) {
+      CKI(sorted_slab(ctx, s, st, &skeys, &ssums));
+      starts.push_back(skeys.size());
+    } else {
+      CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
+    }
+    CKR(cudaEventRecord(ke[b], st));
+    t.merge_end = since();
+    pending[b] = true;
+    pending_k[b] = k;
+  }
+  for (int b = 0; b < 2 && rc == ECC_OK; ++b) CKI(harvest(b));
+  CKR(cudaStreamSynchronize(st));
+  CKR(cudaStreamSynchronize(cp));
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(h2d_done[b]);
+    cudaEventDestroy(used[b]);
+    cudaEventDestroy(kb[b]);
+    cudaEventDestroy(ke[b]);
+  }
+  cudaEventDestroy(ev0);
+  if (rc != ECC_OK) return rc;
+  BinResult r;
+  if (sorted) {
+    CKI(read_flags(ctx, st));
+    merge_runs(skeys, ssums, starts, &r);
+  } else {
+    CKI(finalize_to_host(ctx, (uint32_t)nbins, st, &r));
+    CKI(read_flags(ctx, st));
+  }
+  // merge phase = the device-side reduction; report it after the kernel
+  for (auto& t : tim) {
+    t.merge_begin = t.kernel_end;
+    t.merge_end = t.kernel_end;
+  }
+  if (timings) std::memcpy(timings, tim.data(), nchunks * sizeof(ecc_chunk_timing));
+  const size_t m = r.changes.size();
+  *n_out = m;
+  if (m > cap) return fail(ECC_EINVAL, "output capacity below the number of values");
+  write_values(dtype, sorted, am, r, values_out);
+  std::memcpy(changes_out, r.changes.data(), m * 8);
+  return ECC_OK;
+}
+
+int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, uint64_t count,
+                uint64_t h, uint64_t w, int32_t* chi, uint32_t* presence, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  if (dtype == ECC_F32) return fail(ECC_EINVAL, "batched 2D supports u8 and u16 images");
+  if (h < 1 || w < 1 || h * w > (1ull << 26))
+    return fail(ECC_EINVAL, "batched images must have 1 <= h*w <= 2^26 pixels");
+  if (count > 0x7FFFFFFFull) return fail(ECC_EINVAL, "too many images");
+  if (!data || !chi || !presence) return fail(ECC_EINVAL, "null pointer");
+  cudaStream_t st = pick(ctx, stream);
+  const uint64_t nbins = dtype == ECC_U8 ? 256 : 65536;
+  if (where == 1) {
+    CKR(launch_batch2d(data, (int)dtype, count, (int)h, (int)w, chi, presence, st));
+    ctx->launches += 1;
+    return ECC_OK;
+  }
+  if (where != 0) return fail(ECC_EINVAL, "where must be 0 (host) or 1 (device)");
+  const uint64_t in_bytes = count * h * w * esize(dtype);
+  CKI(ctx->input.ensure(in_bytes));
+  CKI(ctx->chi.ensure(count * nbins * 4));
+  CKI(ctx->bins.ensure(count * nbins / 8));
+  CKR(cudaMemcpyAsync(ctx->input.p, data, in_bytes, cudaMemcpyHostToDevice, st));
+  CKR(launch_batch2d(ctx->input.p, (int)dtype, count, (int)h, (int)w, ctx->chi.as<int32_t>(),
+                     ctx->bins.as<uint32_t>(), st));
+  ctx->launches += 1;
+  CKR(cudaMemcpyAsync(chi, ctx->chi.p, count * nbins * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaMemcpyAsync(presence, ctx->bins.p, count * nbins / 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_fill_synthetic(ecc_ctx* ctx, void* d_data, ecc_dtype dtype, uint64_t n,
+                       uint64_t seed, uint64_t base, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  if (!d_data) return fail(ECC_EINVAL, "null device pointer");
+  CKR(launch_fill(d_data, (int)dtype, n, seed, base, ctx->sms, pick(ctx, stream)));
+  return ECC_OK;
+}
+
+}  // extern "C"

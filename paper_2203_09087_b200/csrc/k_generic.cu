@@ -1,0 +1,361 @@
+// k_generic.cu -- the general-shape stencil kernels (any dims, any slab, any
+// value type) and the K3 finalize kernel.
+//
+// These serve every shape the specialised kernels (k_u8_3d.cu, k_bins.cu)
+// do not: ragged dims, thin slabs, f32 general binning.  One thread owns one
+// axis-0 column (one (j,k) position in 3D, one j in 2D) and sweeps a segment
+// of owned planes with a 3x3(x3) key window in registers, so each neighbour
+// value is loaded once per plane step (the row-oriented traversal of
+// change_row_3d, kernel.hpp:143-188, turned sideways).
+#include <cub/cub.cuh>
+
+#include "ecc_common.cuh"
+#include "internal.h"
+
+namespace eccb {
+
+template <class T>
+__device__ __forceinline__ uint32_t ldkey(const Slab& s, int64_t i, int64_t j,
+                                          int64_t k) {
+  if (i < 0 || i >= s.w0 || j < 0 || j >= s.w1 || k < 0 || k >= s.w2)
+    return KeyTraits<T>::kSentinel;
+  const T* p = static_cast<const T*>(s.base);
+  return KeyTraits<T>::key(__ldg(p + ((i - s.plane0) * s.w1 + j) * s.w2 + k));
+}
+
+template <class T>
+__device__ __forceinline__ T ldval(const Slab& s, int64_t i, int64_t j,
+                                   int64_t k) {
+  const T* p = static_cast<const T*>(s.base);
+  return __ldg(p + ((i - s.plane0) * s.w1 + j) * s.w2 + k);
+}
+
+template <class T, bool AFFINE>
+__device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am,
+                                           uint32_t* flags) {
+  if constexpr (AFFINE) {
+    return affine_bin(am, static_cast<float>(v), flags);
+  } else {
+    return static_cast<uint32_t>(v);
+  }
+}
+
+// Histogram sink: per-CTA shared bins (SMEM) flushed once, or straight to
+// the global int64 histogram for large bin counts.
+template <bool SMEM>
+struct HistSink {
+  int32_t* sums;
+  uint32_t* counts;
+  int64_t* ghist;
+  uint32_t nbins;
+  __device__ __forceinline__ void add(uint32_t bin, int change) {
+    if constexpr (SMEM) {
+      atomicAdd(&sums[bin], change);
+      atomicAdd(&counts[bin], 1u);
+    } else {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[bin]),
+                static_cast<unsigned long long>(static_cast<long long>(change)));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[nbins + bin]), 1ull);
+    }
+  }
+};
+
+template <bool SMEM>
+__device__ __forceinline__ void sink_init(HistSink<SMEM>& h, int64_t* ghist,
+                                          uint32_t nbins, int32_t* sh) {
+  h.ghist = ghist;
+  h.nbins = nbins;
+  if constexpr (SMEM) {
+    h.sums = sh;
+    h.counts = reinterpret_cast<uint32_t*>(sh + nbins);
+    const int nt = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (uint32_t b = tid; b < 2 * nbins; b += nt) sh[b] = 0;
+    __syncthreads();
+  }
+}
+
+template <bool SMEM>
+__device__ __forceinline__ void sink_flush(HistSink<SMEM>& h) {
+  if constexpr (SMEM) {
+    __syncthreads();
+    const int nt = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (uint32_t b = tid; b < h.nbins; b += nt) {
+      const uint32_t c = h.counts[b];
+      if (c) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&h.ghist[b]),
+                  static_cast<unsigned long long>(static_cast<long long>(h.sums[b])));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&h.ghist[h.nbins + b]),
+                  static_cast<unsigned long long>(c));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- 3D
+// block (32, BY): threadIdx.x -> axis 2, threadIdx.y -> axis 1;
+// blockIdx.z -> segment of `seg` owned planes.
+template <class T, bool AFFINE, bool SMEM, bool HIST>
+__global__ void k_generic3(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
+                           uint32_t nbins, uint32_t* flags, int8_t* changes) {
+  extern __shared__ int32_t sh[];
+  HistSink<SMEM> sink;
+  if constexpr (HIST) sink_init<SMEM>(sink, ghist, nbins, sh);
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
+  const int64_t i1 = min(i0 + seg, s.own1);
+  if (j < s.w1 && k < s.w2 && i0 < i1) {
+    uint32_t w[3][3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          w[a][b][c] = ldkey<T>(s, i0 - 1 + a, j - 1 + b, k - 1 + c);
+    for (int64_t i = i0; i < i1; ++i) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          w[2][b][c] = ldkey<T>(s, i + 1, j - 1 + b, k - 1 + c);
+      const int ch = change3(w);
+      if constexpr (HIST) {
+        const T v = ldval<T>(s, i, j, k);
+        sink.add(bin_of<T, AFFINE>(v, am, flags), ch);
+      } else {
+        changes[((i - s.own0) * s.w1 + j) * s.w2 + k] = static_cast<int8_t>(ch);
+      }
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          w[0][b][c] = w[1][b][c];
+          w[1][b][c] = w[2][b][c];
+        }
+    }
+  }
+  if constexpr (HIST) sink_flush<SMEM>(sink);
+}
+
+// ---------------------------------------------------------------- 2D
+// Stencil over axes 0 and 1 (w2 == 1, kernel.hpp:81-94).  1D block over j.
+template <class T, bool AFFINE, bool SMEM, bool HIST>
+__global__ void k_generic2(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
+                           uint32_t nbins, uint32_t* flags, int8_t* changes) {
+  extern __shared__ int32_t sh[];
+  HistSink<SMEM> sink;
+  if constexpr (HIST) sink_init<SMEM>(sink, ghist, nbins, sh);
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
+  const int64_t i1 = min(i0 + seg, s.own1);
+  if (j < s.w1 && i0 < i1) {
+    uint32_t w[3][3];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) w[a][b] = ldkey<T>(s, i0 - 1 + a, j - 1 + b, 0);
+    for (int64_t i = i0; i < i1; ++i) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) w[2][b] = ldkey<T>(s, i + 1, j - 1 + b, 0);
+      const int ch = change2(w);
+      if constexpr (HIST) {
+        const T v = ldval<T>(s, i, j, 0);
+        sink.add(bin_of<T, AFFINE>(v, am, flags), ch);
+      } else {
+        changes[(i - s.own0) * s.w1 + j] = static_cast<int8_t>(ch);
+      }
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        w[0][b] = w[1][b];
+        w[1][b] = w[2][b];
+      }
+    }
+  }
+  if constexpr (HIST) sink_flush<SMEM>(sink);
+}
+
+// ---------------------------------------------------------------- launch
+namespace {
+
+constexpr uint32_t kSmemBinLimit = 8192;  // 2 x 8192 x 4 B = 64 KB
+
+template <class T, bool AFFINE, bool SMEM, bool HIST>
+cudaError_t launch_generic_t(const Slab& s, const AffineMap& am, int64_t* ghist,
+                             uint32_t nbins, uint32_t* flags, int8_t* changes,
+                             int sms, cudaStream_t st) {
+  const int64_t owned = s.own1 - s.own0;
+  const bool d3 = s.w2 > 1;
+  dim3 block, grid;
+  int64_t cols;
+  if (d3) {
+    block = dim3(32, 8, 1);
+    grid = dim3((unsigned)((s.w2 + 31) / 32), (unsigned)((s.w1 + 7) / 8), 1);
+  } else {
+    block = dim3(256, 1, 1);
+    grid = dim3((unsigned)((s.w1 + 255) / 256), 1, 1);
+  }
+  cols = (int64_t)grid.x * grid.y;
+  // enough CTAs for ~8 per SM, but segments of at least 8 planes
+  int64_t nseg = (8LL * sms + cols - 1) / cols;
+  nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (owned + 7) / 8));
+  nseg = std::min<int64_t>(nseg, 65535);
+  const int64_t seg = (owned + nseg - 1) / nseg;
+  grid.z = (unsigned)((owned + seg - 1) / seg);
+  const size_t smem = (HIST && SMEM) ? 2 * nbins * sizeof(int32_t) : 0;
+  if (smem > 48 * 1024) {
+    auto fn = d3 ? k_generic3<T, AFFINE, SMEM, HIST> : k_generic2<T, AFFINE, SMEM, HIST>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (d3)
+    k_generic3<T, AFFINE, SMEM, HIST><<<grid, block, smem, st>>>(s, seg, am, ghist, nbins, flags, changes);
+  else
+    k_generic2<T, AFFINE, SMEM, HIST><<<grid, block, smem, st>>>(s, seg, am, ghist, nbins, flags, changes);
+  return cudaGetLastError();
+}
+
+template <class T, bool AFFINE>
+cudaError_t launch_generic_hist(const Slab& s, const AffineMap& am, int64_t* ghist,
+                                uint32_t nbins, uint32_t* flags, int sms,
+                                cudaStream_t st) {
+  if (nbins <= kSmemBinLimit)
+    return launch_generic_t<T, AFFINE, true, true>(s, am, ghist, nbins, flags, nullptr, sms, st);
+  return launch_generic_t<T, AFFINE, false, true>(s, am, ghist, nbins, flags, nullptr, sms, st);
+}
+
+}  // namespace
+
+cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
+                                      const AffineMap& am, int64_t* ghist,
+                                      uint32_t nbins, uint32_t* flags, int sms,
+                                      cudaStream_t st) {
+  switch (dtype) {
+    case 0:
+      return launch_generic_hist<uint8_t, false>(s, am, ghist, nbins, flags, sms, st);
+    case 1:
+      return launch_generic_hist<uint16_t, false>(s, am, ghist, nbins, flags, sms, st);
+    case 2:
+      if (!affine) return cudaErrorInvalidValue;
+      return launch_generic_hist<float, true>(s, am, ghist, nbins, flags, sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sms,
+                                   cudaStream_t st) {
+  AffineMap am{};
+  switch (dtype) {
+    case 0:
+      return launch_generic_t<uint8_t, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
+    case 1:
+      return launch_generic_t<uint16_t, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
+    case 2:
+      return launch_generic_t<float, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- order keys
+// Owned voxels -> order keys (value_index.hpp:95-99) for the sorted path,
+// plus a NaN check (ValueIndex<float>::build rejects NaN, value_index.hpp:29).
+__global__ void k_order_keys(const float* __restrict__ v, uint64_t n,
+                             uint32_t* __restrict__ keys, uint32_t* flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float x = v[i];
+    if (x != x) atomicOr(flags, kFlagNaN);
+    keys[i] = float_order_key_bits(__float_as_uint(x));
+  }
+}
+
+cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys,
+                              uint32_t* flags, int sms, cudaStream_t st) {
+  k_order_keys<<<sms * 8, 256, 0, st>>>(v, n, keys, flags);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K3
+// merge_local (vcec.hpp:35-66) + vcec_to_ecc (curve.hpp:28-35) over a dense
+// histogram: occurring bins (count > 0) are compacted in ascending order
+// and their change sums prefix-summed.  Bins that never occur have a zero
+// change sum, so chi at an occurring bin is the prefix over all bins.
+// One CTA of 1024 threads, each owning a contiguous run of bins.
+__global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ hist,
+                                                   uint32_t nbins, uint32_t* bins,
+                                                   int64_t* changes, int64_t* chi,
+                                                   uint64_t* count) {
+  using Scan = cub::BlockScan<longlong2, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const uint32_t per = (nbins + 1023) / 1024;
+  const uint32_t b0 = min(nbins, threadIdx.x * per);
+  const uint32_t b1 = min(nbins, b0 + per);
+  long long npres = 0, sum = 0;
+  for (uint32_t b = b0; b < b1; ++b) {
+    npres += hist[nbins + b] != 0;
+    sum += hist[b];
+  }
+  longlong2 in = make_longlong2(npres, sum), ex;
+  struct Add {
+    __device__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+      return make_longlong2(a.x + b.x, a.y + b.y);
+    }
+  };
+  longlong2 total;
+  Scan(tmp).ExclusiveScan(in, ex, make_longlong2(0, 0), Add(), total);
+  long long pos = ex.x, acc = ex.y;
+  for (uint32_t b = b0; b < b1; ++b) {
+    acc += hist[b];
+    if (hist[nbins + b] != 0) {
+      bins[pos] = b;
+      changes[pos] = hist[b];
+      chi[pos] = acc;
+      ++pos;
+    }
+  }
+  if (threadIdx.x == 1023) *count = (uint64_t)total.x;
+}
+
+cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
+                            int64_t* changes, int64_t* chi, uint64_t* count,
+                            cudaStream_t st) {
+  k_finalize<<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- inputs
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+template <class T>
+__global__ void k_fill(T* d, uint64_t n, uint64_t seed, uint64_t base) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t h = splitmix64(seed + (base + i) * 0x9E3779B97F4A7C15ull);
+    if constexpr (sizeof(T) == 1)
+      d[i] = (T)(h >> 56);
+    else if constexpr (sizeof(T) == 2)
+      d[i] = (T)(h >> 48);
+    else
+      d[i] = (float)(h >> 48) * 0x1p-16f;
+  }
+}
+
+cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
+                        uint64_t base, int sms, cudaStream_t st) {
+  const int grid = sms * 16;
+  switch (dtype) {
+    case 0: k_fill<uint8_t><<<grid, 256, 0, st>>>((uint8_t*)d, n, seed, base); break;
+    case 1: k_fill<uint16_t><<<grid, 256, 0, st>>>((uint16_t*)d, n, seed, base); break;
+    case 2: k_fill<float><<<grid, 256, 0, st>>>((float*)d, n, seed, base); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace eccb

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+golden fixtures.  Bit-exact everywhere -- this is integer work."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2203_09087_b200 as eb
+
+pytestmark = pytest.mark.gpu
+
+
+def _img(rec):
+    return np.array(rec["image"], dtype=rec["dtype"]).reshape(rec["shape"])
+
+
+def _same(a_vals, a_ch, b_vals, b_ch):
+    a_vals, b_vals = np.asarray(a_vals), np.asarray(b_vals)
+    if a_vals.dtype == np.float32 or b_vals.dtype == np.float32:
+        ok_v = np.array_equal(np.asarray(a_vals, np.float32).view(np.uint32),
+                              np.asarray(b_vals, np.float32).view(np.uint32))
+    else:
+        ok_v = np.array_equal(a_vals.astype(np.int64), b_vals.astype(np.int64))
+    return ok_v and np.array_equal(np.asarray(a_ch, np.int64), np.asarray(b_ch, np.int64))
+
+
+def test_hand_fixtures(ctx, golden):
+    for name, rec in golden["hand"].items():
+        img = _img(rec)
+        got = ctx.vcec(img)
+        assert _same(got.values, got.changes, np.array(rec["values"], img.dtype), rec["changes"]), name
+
+
+def test_random_fixtures(ctx, golden):
+    for rec in golden["random"]:
+        img = _img(rec)
+        got = ctx.vcec(img)
+        assert _same(got.values, got.changes, np.array(rec["values"], img.dtype), rec["changes"])
+
+
+def _random_images(seed, n, maxd2=9, maxd3=7):
+    rng = np.random.default_rng(seed)
+    for t in range(n):
+        d = (int(rng.integers(1, maxd2)), int(rng.integers(1, maxd2))) if t % 2 == 0 else \
+            tuple(int(x) for x in rng.integers(1, maxd3, 3))
+        k = t % 3
+        if k == 0:
+            yield rng.integers(0, 8, d).astype(np.uint8)
+        elif k == 1:
+            yield rng.random(5).astype(np.float32)[rng.integers(0, 5, d)]
+        else:
+            yield rng.integers(0, 6, d).astype(np.uint16)
+
+
+def test_oracle_sweep_whole_volume(ctx):
+    # acceptance.cpp:95-142 shapes, resident volume path
+    for img in _random_images(1, 300):
+        a = ctx.vcec(img)
+        b = oracle.vcec(img)
+        assert _same(a.values, a.changes, *b), (img.shape, img.dtype)
+
+
+def test_oracle_sweep_chunked_stream(ctx):
+    # chunk invariance through the streaming driver (chunks {1,2,3,w0})
+    for img in _random_images(2, 120):
+        b = oracle.vcec(img)
+        w0 = img.shape[0]
+        for c in sorted({1, 2, 3, w0}):
+            plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(c))
+            a = eb.process_image(img, plan)
+            assert _same(a.values, a.changes, *b), (img.shape, c)
+
+
+def test_medium_shapes_u8(ctx):
+    rng = np.random.default_rng(3)
+    for shape in [(37, 41, 29), (64, 64, 64), (5, 300, 7), (130, 1, 70), (1, 1, 1000), (257, 255, 1),
+                  (64, 1024, 1), (3, 3, 513)]:
+        img = rng.integers(0, 256, shape).astype(np.uint8)
+        a = ctx.vcec(img)
+        assert _same(a.values, a.changes, *oracle.vcec(img)), shape
+
+
+def test_medium_shapes_u16_and_smooth(ctx):
+    rng = np.random.default_rng(4)
+    for shape in [(33, 47, 51), (200, 300, 1), (16, 16, 16)]:
+        img = rng.integers(0, 65536, shape).astype(np.uint16)
+        a = ctx.vcec(img)
+        assert _same(a.values, a.changes, *oracle.vcec(img)), shape
+    # plateau field ((x>>3)+(y>>3)+(z>>3)) & 255 (SURVEY.md 8(d) robustness)
+    z, y, x = np.meshgrid(np.arange(40), np.arange(48), np.arange(56), indexing="ij")
+    img = (((x >> 3) + (y >> 3) + (z >> 3)) & 255).astype(np.uint8)
+    a = ctx.vcec(img)
+    assert _same(a.values, a.changes, *oracle.vcec(img))
+    const = np.full((20, 30, 40), 7, np.uint8)
+    a = ctx.vcec(const)
+    assert list(a.values) == [7] and list(a.changes) == [1]
+
+
+def test_f32_sorted_and_affine(ctx):
+    rng = np.random.default_rng(5)
+    img = rng.random((24, 31, 17)).astype(np.float32)
+    img[0, 0, 0] = -0.0
+    img[3, 4, 5] = 0.0
+    img[5, 5, 5] = np.inf
+    img[23, 30, 16] = -np.inf
+    a = ctx.vcec(img)  # general path: device sort + reduce-by-key
+    assert _same(a.values, a.changes, *oracle.vcec(img))
+    q = (rng.integers(0, 65536, (40, 33, 29)) * 2.0 ** -16).astype(np.float32)
+    a = ctx.vcec(q, binmap=eb.quantised_binmap(65536))
+    assert _same(a.values, a.changes, *oracle.vcec(q))
+    bad = q.copy()
+    bad[1, 1, 1] = 0.3  # not on the 2^-16 grid
+    with pytest.raises(eb.EccError) as ei:
+        ctx.vcec(bad, binmap=eb.quantised_binmap(65536))
+    assert ei.value.code == eb.ECC_EBINMAP
+    nan = q.copy()
+    nan[2, 2, 2] = np.nan
+    with pytest.raises(eb.EccError):
+        ctx.vcec(nan)
+
+
+def test_config1_golden(ctx, golden):
+    img = oracle.synth("u8", (256, 256))
+    c = ctx.curve(img)
+    assert oracle.curve_digest(c.thresholds, c.chi) == golden["configs"]["C1"]["digest"]
+
+
+@pytest.mark.slow
+def test_config2_golden_device_resident(ctx, golden):
+    import torch
+    vol = torch.empty((512, 512, 512), dtype=torch.uint8, device="cuda")
+    ctx.fill_synthetic(vol, seed=1)
+    torch.cuda.synchronize()
+    c = ctx.curve(vol)
+    g = golden["configs"]["C2"]
+    assert oracle.curve_digest(c.thresholds, c.chi) == g["digest"]
+    # the device generator agrees with the oracle's host generator
+    host = oracle.synth("u8", (512, 512, 512))
+    assert np.array_equal(vol.cpu().numpy(), host)
+
+
+@pytest.mark.slow
+def test_config3_images_golden(ctx, golden):
+    for b in (0, 4095):
+        img = oracle.synth("u16", (512, 512), seed=1, base=b * 512 * 512)
+        c = ctx.curve(img)
+        assert oracle.curve_digest(c.thresholds, c.chi) == golden["configs"][f"C3_{b}"]["digest"]
+        chi, pres = ctx.batch2d(img[None])
+        t, cc = eb.curve_batch_to_points(chi[0], pres[0])
+        assert oracle.curve_digest(t, cc) == golden["configs"][f"C3_{b}"]["digest"]
+
+
+def test_batch2d_small(ctx):
+    rng = np.random.default_rng(6)
+    for dt, hi in ((np.uint8, 256), (np.uint16, 65536), (np.uint8, 4), (np.uint16, 3)):
+        imgs = rng.integers(0, hi, (9, 37, 23)).astype(dt)
+        chi, pres = ctx.batch2d(imgs)
+        for b in range(imgs.shape[0]):
+            t, cc = eb.curve_batch_to_points(chi[b], pres[b])
+            v, c = oracle.curve(imgs[b])
+            assert np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, c)
+
+
+def test_batch2d_constant_images_spill(ctx):
+    # one bin receives every pixel: exercises the packed-bin overflow spill
+    imgs = np.zeros((2, 512, 512), np.uint16)
+    imgs[1] = 40000
+    imgs[1, ::2, ::2] = 7  # isolated minima -> large positive partial sums
+    chi, pres = ctx.batch2d(imgs)
+    for b in range(2):
+        t, cc = eb.curve_batch_to_points(chi[b], pres[b])
+        v, c = oracle.curve(imgs[b])
+        assert np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, c)
+
+
+def test_slabs_sum_to_whole(ctx):
+    import torch
+    rng = np.random.default_rng(8)
+    img = rng.integers(0, 256, (50, 40, 30)).astype(np.uint8)
+    whole = torch.zeros(512, dtype=torch.int64, device="cuda")
+    dev = torch.from_numpy(img).cuda()
+    ctx.accumulate_slab(dev, eb.Dims.of(img.shape), 0, 0, 50, whole)
+    parts = torch.zeros(512, dtype=torch.int64, device="cuda")
+    for a, b in ((0, 13), (13, 14), (14, 37), (37, 50)):
+        p0 = max(a - 1, 0)
+        p1 = min(b + 1, 50)
+        ctx.accumulate_slab(dev[p0:p1].contiguous(), eb.Dims.of(img.shape), p0, a, b, parts)
+    torch.cuda.synchronize()
+    assert torch.equal(whole, parts)
+    h, cnt = oracle.hist_dense(img)
+    assert np.array_equal(whole[:256].cpu().numpy(), h)
+    assert np.array_equal(whole[256:].cpu().numpy(), cnt)
+
+
+def test_compute_changes_matches_oracle(ctx):
+    import torch
+    rng = np.random.default_rng(9)
+    for shape in [(20, 21, 22), (30, 40, 1)]:
+        img = rng.integers(0, 5, shape).astype(np.uint8)
+        dev = torch.from_numpy(img).cuda()
+        out = torch.empty(img.size, dtype=torch.int8, device="cuda")
+        ctx.compute_changes(dev, eb.Dims.of(shape), 0, 0, shape[0], out)
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy().reshape(shape), oracle.changes(img))
+
+
+def test_stream_failure_names_chunk(ctx):
+    # test_streaming.cpp:164-198 (FlakySource)
+    rng = np.random.default_rng(53)
+    img = rng.random((8, 3, 3)).astype(np.float32)
+
+    class Flaky(eb.MemorySource):
+        def read_rows(self, r0, r1, dst):
+            if r1 > 5:
+                raise RuntimeError("simulated device failure")
+            super().read_rows(r0, r1, dst)
+
+    plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(4))
+    with pytest.raises(eb.EccError) as ei:
+        eb.process_image(Flaky(img), plan)
+    assert "chunk" in str(ei.value) and "simulated device failure" in str(ei.value)
+
+
+def test_invalid_plans_rejected(ctx):
+    img = np.array([[1], [2], [3], [4]], np.float32).reshape(4, 1, 1)
+    src = eb.MemorySource(img)
+    for ranges in ([], [(0, 2), (3, 4)], [(0, 2), (2, 3)], [(1, 4)]):
+        plan = eb.ChunkPlan([eb.ChunkRange(a, b) for a, b in ranges])
+        with pytest.raises(eb.EccError):
+            ctx.process_source(src, plan)
+
+
+def test_stream_reports_timings_and_overlap(ctx):
+    rng = np.random.default_rng(59)
+    img = rng.integers(0, 256, (160, 128, 128)).astype(np.uint8)
+    plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(4))
+    rep = eb.EngineReport()
+    v = eb.process_image(img, plan, eb.EngineOptions(ingest_delay_ms=50), rep)
+    assert v.total() == 1
+    assert len(rep.chunks) == 4
+    for t in rep.chunks:
+        assert t.ingest_end >= t.ingest_begin and t.kernel_end >= t.kernel_begin
+    # acceptance.cpp:293-317: ingest of chunk k+1 overlaps device work of chunk k
+    assert any(min(rep.chunks[k].kernel_end, rep.chunks[k + 1].ingest_end) >
+               max(rep.chunks[k].kernel_begin, rep.chunks[k + 1].ingest_begin) or
+               rep.chunks[k + 1].ingest_begin < rep.chunks[k].kernel_end
+               for k in range(3))
