@@ -26,6 +26,8 @@ cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
                                    const AffineMap& am, int64_t* ghist,
                                    uint32_t nbins, uint32_t* flags, int sms,
                                    cudaStream_t st, bool* handled);
+cudaError_t launch_changes_fast(const Slab& s, int dtype, int8_t* out, int sms, cudaStream_t st,
+                                bool* handled);
 }  // namespace eccb
 
 namespace {
@@ -498,7 +500,9 @@ int ecc_compute_changes(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
   CKI(check_slab(image, plane0, nplanes, own0, own1));
   if (!d_planes || !d_out) return fail(ECC_EINVAL, "null device pointer");
   const Slab s = make_slab(d_planes, image, plane0, nplanes, own0, own1);
-  CKR(launch_generic_changes(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream)));
+  bool handled = false;
+  CKR(launch_changes_fast(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream), &handled));
+  if (!handled) CKR(launch_generic_changes(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream)));
   ctx->launches += 1;
   return ECC_OK;
 }
@@ -608,6 +612,9 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     CKR(cudaEventCreate(&ke[b]));
   }
   CKR(cudaEventRecord(ev0, st));
+  // map device event times onto the host clock of the ChunkTiming fields
+  CKR(cudaEventSynchronize(ev0));
+  const double t_ev0 = since();
   std::vector<uint32_t> skeys;
   std::vector<int64_t> ssums;
   std::vector<size_t> starts{0};
@@ -624,8 +631,8 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     CKR(cudaEventElapsedTime(&a, ev0, kb[b]));
     CKR(cudaEventElapsedTime(&c, ev0, ke[b]));
     ecc_chunk_timing& t = tim[pending_k[b]];
-    t.kernel_begin = a * 1e-3;
-    t.kernel_end = c * 1e-3;
+    t.kernel_begin = t_ev0 + a * 1e-3;
+    t.kernel_end = t_ev0 + c * 1e-3;
     pending[b] = false;
     return ECC_OK;
   };

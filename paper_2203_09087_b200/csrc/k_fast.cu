@@ -1,16 +1,32 @@
-// k_fast.cu -- dispatch to the shape-specialised kernels (filled in as they
-// land); returns handled = false when the generic kernel must run.
+// k_fast.cu -- dispatch to the shape-specialised kernels; returns
+// handled = false when the generic kernel (k_generic.cu) must run.
 #include "internal.h"
 
 namespace eccb {
+
+bool u8_3d_supported(const Slab& s);
+cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st);
 
 cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
                                    const AffineMap& am, int64_t* ghist,
                                    uint32_t nbins, uint32_t* flags, int sms,
                                    cudaStream_t st, bool* handled) {
-  (void)s; (void)dtype; (void)affine; (void)am; (void)ghist; (void)nbins;
-  (void)flags; (void)sms; (void)st;
+  (void)am; (void)flags;
   *handled = false;
+  if (dtype == 0 && !affine && nbins == 256 && u8_3d_supported(s)) {
+    *handled = true;
+    return launch_u8_3d(s, ghist, nullptr, sms, st);
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_changes_fast(const Slab& s, int dtype, int8_t* out, int sms, cudaStream_t st,
+                                bool* handled) {
+  *handled = false;
+  if (dtype == 0 && u8_3d_supported(s)) {
+    *handled = true;
+    return launch_u8_3d(s, nullptr, out, sms, st);
+  }
   return cudaSuccess;
 }
 

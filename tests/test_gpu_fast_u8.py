@@ -1,0 +1,85 @@
+"""GPU parity of the bit-sliced 3D u8 kernel (k_u8_3d.cu) against the oracle.
+
+The kernel serves 3D u8 volumes whose axis-2 rows are a multiple of 16
+bytes; it tiles axes 1/2 into 30x30 columns with a 1-voxel halo and splits
+the (column, plane) work evenly over warps, so the cases below target column
+edges, uneven splits, tiny dims, slabs, ties around 255 (the collar value)
+and constant / plateau inputs.  Bit-exact.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2203_09087_b200 as eb
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(ctx, img):
+    a = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(a.values.astype(np.int64), v.astype(np.int64)), img.shape
+    assert np.array_equal(a.changes, c), img.shape
+
+
+@pytest.mark.parametrize("shape", [
+    (1, 1, 16), (1, 2, 16), (2, 1, 32), (3, 30, 32), (4, 31, 16), (5, 32, 48), (7, 61, 64),
+    (9, 60, 96), (33, 29, 32), (17, 90, 128), (64, 64, 64), (40, 100, 160), (2, 512, 512),
+    (31, 17, 240), (8, 3, 496),
+])
+def test_random_shapes(ctx, shape):
+    rng = np.random.default_rng(sum(shape))
+    _check(ctx, rng.integers(0, 256, shape).astype(np.uint8))
+
+
+@pytest.mark.parametrize("lo,hi", [(250, 256), (0, 2), (254, 256), (100, 104)])
+def test_ties_and_collar_values(ctx, lo, hi):
+    # many ties, and values equal to the 255 the kernel uses for the collar
+    rng = np.random.default_rng(lo)
+    for shape in [(6, 35, 48), (12, 62, 32), (3, 5, 16)]:
+        _check(ctx, rng.integers(lo, hi, shape).astype(np.uint8))
+
+
+def test_constant_and_plateau(ctx):
+    for val in (0, 255, 77):
+        img = np.full((13, 47, 64), val, np.uint8)
+        a = ctx.vcec(img)
+        assert list(a.values) == [val] and list(a.changes) == [1]
+    z, y, x = np.meshgrid(np.arange(40), np.arange(70), np.arange(96), indexing="ij")
+    img = (((x >> 3) + (y >> 3) + (z >> 3)) & 255).astype(np.uint8)
+    _check(ctx, img)
+    # large constant run: exercises the histogram drain (>5000 voxels per bin)
+    img = np.full((64, 128, 128), 9, np.uint8)
+    img[::7, ::5, ::3] = 200
+    _check(ctx, img)
+
+
+def test_slabs_match_whole(ctx):
+    """ecc_accumulate_slab over z-slabs with halo planes sums to the whole."""
+    import torch
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 256, (50, 70, 80)).astype(np.uint8)
+    want = oracle.vcec(img)
+    dev = torch.from_numpy(img).cuda()
+    hist = torch.zeros(512, dtype=torch.int64, device="cuda")
+    dims = eb.Dims.of(img.shape)
+    for own0, own1 in [(0, 1), (1, 17), (17, 18), (18, 49), (49, 50)]:
+        p0, p1 = max(own0 - 1, 0), min(own1 + 1, 50)
+        ctx.accumulate_slab(dev[p0:p1].contiguous(), dims, p0, own0, own1, hist)
+    torch.cuda.synchronize()
+    h = hist.cpu().numpy()
+    bins = np.nonzero(h[256:])[0]
+    assert np.array_equal(bins, want[0].astype(np.int64))
+    assert np.array_equal(h[bins], want[1])
+
+
+def test_config2_size_properties(ctx, golden):
+    """Full C2 size: chi ends at 1, first point and the golden curve digest."""
+    import torch
+    dev = torch.empty((512, 512, 512), dtype=torch.uint8, device="cuda")
+    ctx.fill_synthetic(dev, seed=1)
+    torch.cuda.synchronize()
+    cur = ctx.curve(dev)
+    assert int(cur.chi[-1]) == 1 and cur.size() == 256
+    assert int(cur.chi[0]) == 499566
+    assert oracle.curve_digest(cur.thresholds, cur.chi) == golden["configs"]["C2"]["digest"]
