@@ -1,5 +1,5 @@
 // k_u8_3d.cu -- K1+K2 for 3D u8 volumes on sm_100a: bit-sliced tournament
-// stencil + warp-private shared-memory histogram, TMA-fed.
+// stencil + per-CTA (code, value) shared-memory histogram, TMA-fed.
 //
 // Replaces, for u8 3D images, the reference hot loop
 //   run_chunk_kernel_u8 (streaming.hpp:146-174)
@@ -9,24 +9,35 @@
 // for the occurrence list, value_index.hpp:63-71) bit-exactly.
 //
 // Mapping.  A warp owns a "column": 32 rows along axis 1 (one per lane) x
-// 32 voxels along axis 2 (one per bit of a bit plane), and sweeps axis 0.
-// Lane 0 / 31 and bit 0 / 31 are halo, so a column yields up to 30 x 30
-// voxels per plane.  Each plane of a column arrives by one TMA box
-// (48 B x 32 rows) into a per-warp ring; a lane reads its 48-byte row with
-// three conflict-free LDS.128, byte-interleaves and bit-transposes it into
-// 8 bit planes.
+// 32 voxels along axis 2 (one per bit of a bit plane) and sweeps a segment
+// of axis 0.  Lane 0 / 31 and bit 0 / 31 are halo, so a column yields up to
+// 30 x 30 voxels per plane.  Work units are (segment, column) pairs in
+// segment-major order: warps that run at the same time hold neighbouring
+// columns at the same axis-0 position, so the halo rows/bytes a column
+// shares with its neighbours are read from DRAM once and hit in L2 after.
+// Each plane of a column arrives by one TMA box (48 B x 32 rows; the box
+// origin along axis 2 must be 16-byte aligned) into a per-warp ring; a lane
+// reads its 48-byte row with three LDS.128 and funnel-shifts out its
+// 32-byte window, byte-interleaves and bit-transposes it into 8 bit planes.
 //
 // Stencil (validated by tools/tournament_model.py).  With ties going to
 // the earlier voxel (kernel.hpp:21-27), a voxel introduces a face / edge /
 // vertex iff it is the minimum of the 2 / 4 / 8 voxels around it, so the
 // change is  -1 + #2-blocks won - #4-blocks won + #8-blocks won.  Block
-// winners are found by a tournament (z-pairs, y-pairs, x-pairs; yz, xz, xy
-// 4-blocks; the 8-block) -- 7 bit-sliced comparisons and 3 bit-sliced
-// minimum selections per voxel -- and each voxel gathers its 26 "won" bits
-// from its own and its neighbours' tournament results (shifts along z,
-// warp shuffles along y, registers carried along x).  The 26 bits are
-// summed with a bit-sliced carry-save tree, transposed back to bytes and
-// scattered into the histogram as (change + 8) + 2^16 per voxel.
+// winners come from a tournament: 7 bit-sliced comparisons (z, y, yz in the
+// plane; x, xz, xy, xyz against the next plane) and 3 bit-sliced minimum
+// selections per voxel.  The x-side blocks pair up (the block towards x+1
+// and the block towards x-1 share their in-plane factor), so each pair is
+// entered into the sum as a 2-bit number built by two LOP3s; 17 weight-1
+// and 9 weight-2 bit vectors then go through a 19-full-adder carry-save
+// tree (bits::sum_code), giving code = (change + 17) mod 16 per voxel.
+//
+// Histogram (K2).  The 4 code planes are transposed back to bytes and each
+// voxel does ONE shared-memory atomic increment at hist[code][value] (one
+// PRMT builds the index from the value byte and the code byte); the table
+// (16 x 256 x u32 per CTA) is reduced to per-value change sums and counts
+// once at the end and flushed with int64 global atomics.  Voxels the lane
+// does not own go to code 8, which no real change produces.
 //
 // Collar.  Voxels outside the image hold 255 in the planes; that is only
 // wrong when an outside voxel is the EARLIER side of a comparison (the
@@ -35,7 +46,6 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
-#include <cstdlib>
 #include <cstdint>
 
 #include "bits.cuh"
@@ -46,25 +56,29 @@ namespace eccb {
 namespace u83d {
 
 constexpr int NW = 4;      // warps per CTA
-constexpr int NS = 8;      // TMA ring stages per warp
+constexpr int NS = 4;      // TMA ring stages per warp
 constexpr int BOXZ = 48;   // box bytes along axis 2 (window of 32 + alignment)
 constexpr int BOXY = 32;   // rows per box (one per lane)
 constexpr int STAGE = BOXZ * BOXY;
-constexpr int FLUSH_EVERY = 5;  // steps between histogram drains (<= 5041 voxels per bin)
+constexpr int NCODE = 16;
+constexpr int HIST_WORDS = NCODE * 256;
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
-constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + NW * 256 * 4;
-static_assert(NW * 512 * 8 <= RING_BYTES, "reduction scratch aliases the ring");
+constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + HIST_WORDS * 4;
+constexpr int CTAS_PER_SM = 3;
+constexpr uint32_t FULL = 0xFFFFFFFFu;
 
 struct Geom {
-  int W0, W1, W2;     // image dims
-  int plane0;         // image plane held at tensor-map coordinate 0
-  int own0;           // first owned plane
-  int P;              // owned planes
-  int Gy, Gz;         // column groups along axes 1 and 2
-  long long total;    // Gy * Gz * P plane-steps of work
-  int8_t* chg;        // CH mode: per-voxel changes of the owned planes (compute_changes)
-  uint32_t* dbg;      // debug dump (nullptr in production)
+  int W0, W1, W2;  // image dims
+  int plane0;      // image plane held at tensor-map coordinate 0
+  int own0;        // first owned plane
+  int P;           // owned planes
+  int Gy, Gz;      // column groups along axes 1 and 2
+  int ncols;       // Gy * Gz
+  int seglen;      // planes per segment
+  int nunits;      // ncols * segments
+  int8_t* chg;     // CH mode: per-voxel changes of the owned planes (compute_changes)
+  uint32_t four;   // = 4, opaque to ptxas so the histogram address stays an IMAD
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,371 +118,284 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
       : "memory");
 }
 
-// Walks the warp's share [L, Lend) of the linearised (column, plane) work.
-// Each run of consecutive planes of one column costs len + 2 steps (the
-// halo plane on each side along axis 0).
-__device__ __forceinline__ void col_geom(const Geom& g, int col, int& ys, int& ye, int& zs,
-                                         int& ze);
-
+// Position of one warp in its sequence of work units (unit u = gw + i *
+// nwt, segment-major) and of the plane step k in [0, len + 2) within it
+// (one halo plane on each side along axis 0).
 struct Cursor {
-  long long L, Lend;
-  int col, xo, len, k;
-  int ys, zs;  // TMA box origin of the current run's column
-  __device__ __forceinline__ void start(const Geom& g, long long a, long long b) {
-    L = a;
-    Lend = b;
-    k = 0;
-    if (L < Lend) set(g);
-  }
+  int u, k, len, x0, ys, ye, zs, ze;
   __device__ __forceinline__ void set(const Geom& g) {
-    col = (int)(L / g.P);
-    xo = (int)(L - (long long)col * g.P);
-    { const long long r1 = g.P - xo, r2 = Lend - L; len = (int)(r1 < r2 ? r1 : r2); }
-    int ye, ze;
-    col_geom(g, col, ys, ye, zs, ze);
+    const int seg = u / g.ncols, col = u - seg * g.ncols;
+    x0 = g.own0 + seg * g.seglen;
+    len = min(g.seglen, g.P - seg * g.seglen);
+    const int gy = col / g.Gz, gz = col - gy * g.Gz;
+    ys = (int)((long long)gy * g.W1 / g.Gy);
+    ye = (int)((long long)(gy + 1) * g.W1 / g.Gy);
+    zs = (int)((long long)gz * g.W2 / g.Gz);
+    ze = (int)((long long)(gz + 1) * g.W2 / g.Gz);
   }
-  __device__ __forceinline__ bool valid() const { return L < Lend; }
-  __device__ __forceinline__ void next(const Geom& g) {
+  __device__ __forceinline__ void start(const Geom& g, int u0) {
+    u = u0;
+    k = 0;
+    if (u < g.nunits) set(g);
+  }
+  __device__ __forceinline__ bool valid(const Geom& g) const { return u < g.nunits; }
+  __device__ __forceinline__ void next(const Geom& g, int nwt) {
     if (++k == len + 2) {
-      L += len;
+      u += nwt;
       k = 0;
-      if (L < Lend) set(g);
+      if (u < g.nunits) set(g);
     }
   }
 };
 
-// Column geometry: rows [ys, ye) along axis 1 and voxels [zs, ze) along axis
-// 2 are owned; lane l holds row ys - 1 + l, bit p holds voxel zs - 1 + p.
-__device__ __forceinline__ void col_geom(const Geom& g, int col, int& ys, int& ye, int& zs,
-                                         int& ze) {
-  const int gy = col / g.Gz, gz = col - gy * g.Gz;
-  ys = (int)((long long)gy * g.W1 / g.Gy);
-  ye = (int)((long long)(gy + 1) * g.W1 / g.Gy);
-  zs = (int)((long long)gz * g.W2 / g.Gz);
-  ze = (int)((long long)(gz + 1) * g.W2 / g.Gz);
-}
-
-
-// Carried state of one row (the "previous" row of a step).
+// Carried state of one row of a column (plane X-1 while plane X arrives).
 struct Row {
-  uint32_t C[8], mz[8], my[8], myz[8], wv[8];
-  uint32_t bz, by, byz;  // "lower side wins" bits of the row's z/y pairs and yz blocks
-  __device__ __forceinline__ void clear() {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) C[i] = mz[i] = my[i] = myz[i] = wv[i] = 0;
-    bz = by = byz = 0;
-  }
+  uint32_t C[8], mz[8], my[8], myz[8];  // value planes and z / y / yz block minima
+  uint32_t gz, gy, gyz;                 // "upper side wins" bits of the z / y pairs, yz blocks
+  uint32_t W[8];                        // the row's 32 value bytes (natural order)
 };
 
-// x-comparison results at anchors two rows back (row X-2).
+// x-comparison results between planes X-2 and X-1 ("X-1 wins" bits).
 struct XCarry {
-  uint32_t bx, bxz, bxy, b8, bxyu, b8u;
-  __device__ __forceinline__ void clear() { bx = bxz = bxy = b8 = bxyu = b8u = 0; }
+  uint32_t gxa, gxz, gxz1, gxy, gxyu, g8, g81, g8u, g8u1;
+  __device__ __forceinline__ void clear() { gxa = gxz = gxz1 = gxy = gxyu = g8 = g81 = g8u = g8u1 = 0; }
 };
 
-// Per-run (per column) constants.
+// Per-unit constants of this lane.
 struct RunGeom {
-  int y, z0;          // this lane's row, the voxel at bit 0
-  int o;              // byte offset of voxel z0 in the 16-byte aligned box row
-  int ys, zs;         // tile origin for the TMA box
-  uint32_t zout;      // bits whose voxel lies outside [0, W2)
-  uint32_t vmask;     // bits whose change this lane emits (0 for halo lanes)
-  uint32_t vc[8];     // vmask transposed to bytes: byte b of vc[r] = bit 8b + r
-  bool yout;          // this lane's row lies outside [0, W1)
-  __device__ __forceinline__ void set(const Geom& g, int col, int lane) {
-    int ye, ze;
-    col_geom(g, col, ys, ye, zs, ze);
-    y = ys - 1 + lane;
-    z0 = zs - 1;
+  int y;          // this lane's row
+  int o;          // byte offset of the window in the 16-byte aligned box row
+  uint32_t zout;  // bits whose voxel lies outside [0, W2)
+  uint32_t vm;    // bits whose change this lane emits (0 for halo lanes)
+  bool yout;      // this lane's row lies outside [0, W1)
+  bool zlo;       // bit 0 is the z = -1 collar
+  bool edge;      // some lane of the column holds collar voxels (warp-uniform)
+  __device__ __forceinline__ void set(const Geom& g, const Cursor& c, int lane) {
+    y = c.ys - 1 + lane;
+    const int z0 = c.zs - 1;
     o = z0 - ((z0 >> 4) << 4);
     yout = (y < 0) | (y >= g.W1);
-    const int lo = -z0;             // first in-image bit
-    const int hi = g.W2 - z0;       // one past the last in-image bit
-    uint32_t in = 0xFFFFFFFFu;
-    if (lo > 0) in &= 0xFFFFFFFFu << lo;
+    zlo = z0 < 0;
+    const int lo = -z0;         // first in-image bit
+    const int hi = g.W2 - z0;   // one past the last in-image bit
+    uint32_t in = FULL;
+    if (lo > 0) in &= FULL << lo;
     if (hi < 32) in &= (1u << hi) - 1u;
     zout = ~in;
-    const int nz = ze - zs;         // owned bits 1..nz
-    const uint32_t own = ((nz >= 31 ? 0xFFFFFFFFu : ((1u << (nz + 1)) - 1u))) & ~1u;
-    vmask = (lane >= 1 && lane <= ye - ys) ? own : 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) vc[i] = 0;
-    vc[0] = vmask;
-    bits::transpose8(vc);
+    const int nz = c.ze - c.zs;  // owned bits 1..nz
+    const uint32_t own = (nz >= 31 ? FULL : ((1u << (nz + 1)) - 1u)) & ~1u;
+    vm = (lane >= 1 && lane <= c.ye - c.ys) ? own : 0u;
+    edge = __any_sync(FULL, yout | (zout != 0));
   }
 };
+
+__device__ __forceinline__ int decode_change(uint32_t code) {
+  return code >= 10 ? (int)code - 17 : (int)code - 1;
+}
 
 template <bool CH, class Issue>
 __device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunGeom& rg, int& step,
-                                           int& since_flush, uint8_t (*myring)[STAGE],
-                                           uint64_t* myfull, uint32_t* myhist, Cursor& pc,
-                                           int lane, Row& P, Row& N, XCarry& xc, int (&accS)[8],
-                                           uint32_t (&accC)[8], Issue& issue) {
-  const unsigned FULL = 0xFFFFFFFFu;
+                                           uint8_t (*myring)[STAGE], uint64_t* myfull,
+                                           uint32_t* hist, const Cursor& pc, int nwt, int lane,
+                                           Row& P, Row& N, XCarry& xc, Issue& issue) {
   const int slot = step % NS;
   const uint32_t phase = (uint32_t)((step / NS) & 1);
-  const int X = g.own0 + cc.xo - 1 + cc.k;
+  const int X = cc.x0 - 1 + cc.k;
   mbar_wait(&myfull[slot], phase);
-  const uint4* rowp = reinterpret_cast<const uint4*>(myring[slot] + lane * BOXZ);
-  const uint4 q0 = rowp[0], q1 = rowp[1], q2 = rowp[2];
-  const uint32_t W[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
-  // the 32-voxel window starts at byte o (warp-uniform) of the row
-  uint32_t a[8];
-  const int sh = 8 * (rg.o & 3);
-#define ECC_WINDOW(Q)                                                      \
-  _Pragma("unroll") for (int j = 0; j < 8; ++j) a[j] = __funnelshift_r(W[(Q) + j], W[(Q) + j + 1], sh)
-  switch (rg.o >> 2) {
-    case 0: ECC_WINDOW(0); break;
-    case 1: ECC_WINDOW(1); break;
-    case 2: ECC_WINDOW(2); break;
-    default: ECC_WINDOW(3); break;
-  }
+  {
+    const uint4* rowp = reinterpret_cast<const uint4*>(myring[slot] + lane * BOXZ);
+    const uint4 q0 = rowp[0], q1 = rowp[1], q2 = rowp[2];
+    const uint32_t Wd[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                             q2.x, q2.y, q2.z, q2.w};
+    // the 32-voxel window starts at byte o (warp-uniform) of the row
+    const int sh = 8 * (rg.o & 3);
+#define ECC_WINDOW(Q)                                                        \
+  _Pragma("unroll") for (int j = 0; j < 8; ++j) N.W[j] = __funnelshift_r(Wd[(Q) + j], Wd[(Q) + j + 1], sh)
+    switch (rg.o >> 2) {
+      case 0: ECC_WINDOW(0); break;
+      case 1: ECC_WINDOW(1); break;
+      case 2: ECC_WINDOW(2); break;
+      default: ECC_WINDOW(3); break;
+    }
 #undef ECC_WINDOW
-  if (g.dbg && step < 8) {
-    const long long gw = (long long)blockIdx.x * NW + (threadIdx.x >> 5);
-    uint32_t* d = g.dbg + ((gw * 8 + step) * 32 + lane) * 12;
-    for (int j = 0; j < 8; ++j) d[j] = a[j];
-    d[8] = X; d[9] = cc.k; d[10] = slot; d[11] = phase;
   }
   __syncwarp();
-  if (pc.valid()) {  // refill this slot with the load NS steps ahead
+  if (pc.valid(g)) {  // refill this slot with the load NS steps ahead
     if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     issue(slot);
   }
-  bits::byte_interleave(a, N.wv);
   uint32_t (&C)[8] = N.C;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) C[i] = N.wv[i];
+  bits::byte_interleave(N.W, C);
   bits::transpose8(C);
   // collar: voxels outside the image hold 255 (TMA filled zeros)
   const bool xout = (X < 0) | (X >= g.W0);
-  const uint32_t om = (rg.yout | xout) ? FULL : rg.zout;
-  if (__any_sync(FULL, om != 0)) {
+  if (rg.edge | xout) {  // warp-uniform: only columns / planes touching the collar
+    const uint32_t om = (rg.yout | xout) ? FULL : rg.zout;
 #pragma unroll
     for (int i = 0; i < 8; ++i) C[i] |= om;
   }
 
-  // ---- tournament on the new row
-  uint32_t Cz[8], Cy[8], mzy[8];
+  // ---- tournament on the new row (plane X)
+  {
+    uint32_t Cz[8], Cy[8], mzy[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) Cz[i] = C[i] >> 1;
-  uint32_t gz = bits::gt<8>(C, Cz);
-  if (rg.z0 < 0) gz |= 1u;  // z = -1 never wins as the lower side
-  bits::sel<8>(N.mz, gz, C, Cz);
+    for (int i = 0; i < 8; ++i) Cz[i] = C[i] >> 1;
+    uint32_t gz = bits::gt<8>(C, Cz);
+    if (rg.zlo) gz |= 1u;  // z = -1 never wins as the lower side
+    bits::sel<8>(N.mz, gz, C, Cz);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) Cy[i] = __shfl_down_sync(FULL, C[i], 1);
-  uint32_t gy = bits::gt<8>(C, Cy);
-  if (rg.y < 0) gy = FULL;  // y = -1 never wins
-  bits::sel<8>(N.my, gy, C, Cy);
+    for (int i = 0; i < 8; ++i) Cy[i] = __shfl_down_sync(FULL, C[i], 1);
+    uint32_t gy = bits::gt<8>(C, Cy);
+    if (rg.y < 0) gy = FULL;  // y = -1 never wins
+    bits::sel<8>(N.my, gy, C, Cy);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) mzy[i] = __shfl_down_sync(FULL, N.mz[i], 1);
-  uint32_t gyz = bits::gt<8>(N.mz, mzy);
-  if (rg.y < 0) gyz = FULL;
-  bits::sel<8>(N.myz, gyz, N.mz, mzy);
-  N.bz = ~gz;
-  N.by = ~gy;
-  N.byz = ~gyz;
+    for (int i = 0; i < 8; ++i) mzy[i] = __shfl_down_sync(FULL, N.mz[i], 1);
+    uint32_t gyz = bits::gt<8>(N.mz, mzy);
+    if (rg.y < 0) gyz = FULL;
+    bits::sel<8>(N.myz, gyz, N.mz, mzy);
+    N.gz = gz;
+    N.gy = gy;
+    N.gyz = gyz;
+  }
 
   if (cc.k >= 1) {
-    // ---- x comparisons: anchors in row X-1
-    uint32_t bx = ~bits::gt<8>(P.C, C);
-    uint32_t bxz = ~bits::gt<8>(P.mz, N.mz);
-    uint32_t bxy = ~bits::gt<8>(P.my, N.my);
-    uint32_t b8 = ~bits::gt<8>(P.myz, N.myz);
-    if (X - 1 < 0) bx = bxz = bxy = b8 = 0;  // x = -1 never wins
-    const uint32_t bxyu = __shfl_up_sync(FULL, bxy, 1);
-    const uint32_t b8u = __shfl_up_sync(FULL, b8, 1);
+    // ---- x comparisons between planes X-1 (P) and X (N): "X wins" bits
+    uint32_t gxa = bits::gt<8>(P.C, N.C);
+    uint32_t gxz = bits::gt<8>(P.mz, N.mz);
+    uint32_t gxy = bits::gt<8>(P.my, N.my);
+    uint32_t g8 = bits::gt<8>(P.myz, N.myz);
+    if (X - 1 < 0) gxa = gxz = gxy = g8 = FULL;  // x = -1 never wins
+    const uint32_t gxz1 = gxz << 1, g81 = g8 << 1;
+    const uint32_t gxyu = __shfl_up_sync(FULL, gxy, 1);
+    const uint32_t g8u = __shfl_up_sync(FULL, g8, 1);
+    const uint32_t g8u1 = g8u << 1;
     if (cc.k >= 2) {
       // ---- changes of row X-1: each voxel gathers its 26 block wins
-      const uint32_t byu = __shfl_up_sync(FULL, P.by, 1);
-      const uint32_t byzu = __shfl_up_sync(FULL, P.byz, 1);
-      const uint32_t Z0 = P.bz, Z1 = ~(P.bz << 1);
-      const uint32_t Yf0 = P.by, Yf1 = ~byu;
-      const uint32_t Y00 = P.byz, Y01 = P.byz << 1, Y10 = ~byzu, Y11 = ~(byzu << 1);
-      const uint32_t I00 = Z0 & Y00, I01 = Z1 & Y01, I10 = Z0 & Y10, I11 = Z1 & Y11;
-      // 6 faces and 8 vertices count +1, the 12 edges are entered negated
-      uint32_t t[26];
-      t[0] = Z0; t[1] = Z1; t[2] = Yf0; t[3] = Yf1; t[4] = bx; t[5] = ~xc.bx;
-      t[6] = ~I00; t[7] = ~I01; t[8] = ~I10; t[9] = ~I11;
-      t[10] = ~(Z0 & bxz); t[11] = ~(Z1 & (bxz << 1));
-      t[12] = ~(Z0 & ~xc.bxz); t[13] = ~(Z1 & ~(xc.bxz << 1));
-      t[14] = ~(Yf0 & bxy); t[15] = ~(Yf1 & bxyu);
-      t[16] = ~(Yf0 & ~xc.bxy); t[17] = ~(Yf1 & ~xc.bxyu);
-      t[18] = I00 & b8; t[19] = I01 & (b8 << 1); t[20] = I10 & b8u; t[21] = I11 & (b8u << 1);
-      t[22] = I00 & ~xc.b8; t[23] = I01 & ~(xc.b8 << 1); t[24] = I10 & ~xc.b8u;
-      t[25] = I11 & ~(xc.b8u << 1);
-      // S = sum t (0..26);  change + 8 = S - 5 = S + 11 (mod 16)
-      const uint32_t ONE = FULL;
-      uint32_t s1[9], c2[9];
+      const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
+      const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
+      const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;  // wins its z+ / z- pair
+      const uint32_t Yf0 = ~P.gy, Yf1 = gyu;      // wins its y+ / y- pair
+      const uint32_t I00 = Z0 & ~P.gyz;           // wins the four yz 4-blocks
+      const uint32_t I01 = (P.gz & ~P.gyz) << 1;
+      const uint32_t I10 = Z0 & gyzu;
+      const uint32_t I11 = (P.gz & gyzu) << 1;
+      // x-side pairs F * (a + b): sum bit F & (a ^ b), carry bit F & a & b;
+      // the 4 edge pairs enter negated (-e = ~e - 1).
+      uint32_t w1[17], w2[9];
+      w1[0] = Z0; w1[1] = Z1; w1[2] = Yf0; w1[3] = Yf1;
+      w1[4] = ~I00; w1[5] = ~I01; w1[6] = ~I10; w1[7] = ~I11;
+      w1[8] = ~(gxa ^ xc.gxa);          w2[0] = ~gxa & xc.gxa;              // x faces
+      w1[9] = ~(Z0 & ~(gxz ^ xc.gxz));  w2[1] = ~(Z0 & ~gxz & xc.gxz);      // xz edges
+      w1[10] = ~(Z1 & ~(gxz1 ^ xc.gxz1)); w2[2] = ~(Z1 & ~gxz1 & xc.gxz1);
+      w1[11] = ~(Yf0 & ~(gxy ^ xc.gxy)); w2[3] = ~(Yf0 & ~gxy & xc.gxy);   // xy edges
+      w1[12] = ~(Yf1 & ~(gxyu ^ xc.gxyu)); w2[4] = ~(Yf1 & ~gxyu & xc.gxyu);
+      w1[13] = I00 & ~(g8 ^ xc.g8);     w2[5] = I00 & ~g8 & xc.g8;          // vertices
+      w1[14] = I01 & ~(g81 ^ xc.g81);   w2[6] = I01 & ~g81 & xc.g81;
+      w1[15] = I10 & ~(g8u ^ xc.g8u);   w2[7] = I10 & ~g8u & xc.g8u;
+      w1[16] = I11 & ~(g8u1 ^ xc.g8u1); w2[8] = I11 & ~g8u1 & xc.g8u1;
+      // S = change + 17 in [10, 22]; code = S mod 16; non-emitted -> 8
+      uint32_t s[4];
+      bits::sum_code(w1, w2, s);
+      const uint32_t vm = rg.vm;
+      const uint32_t hist_s = smem_u32(hist);
+      uint32_t V[8];
+      bits::transpose_codes(s[0] & vm, s[1] & vm, s[2] & vm, s[3] | ~vm, V);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) bits::fa(t[3 * i], t[3 * i + 1], t[3 * i + 2], s1[i], c2[i]);
-      bits::fa(t[24], t[25], ONE, s1[8], c2[8]);  // +1 at weight 1
-      uint32_t s1b[3], c2b[3];
-#pragma unroll
-      for (int i = 0; i < 3; ++i) bits::fa(s1[3 * i], s1[3 * i + 1], s1[3 * i + 2], s1b[i], c2b[i]);
-      uint32_t bit0, c2c;
-      bits::fa(s1b[0], s1b[1], s1b[2], bit0, c2c);
-      uint32_t s2[4], c4[4];
-      bits::fa(c2[0], c2[1], c2[2], s2[0], c4[0]);
-      bits::fa(c2[3], c2[4], c2[5], s2[1], c4[1]);
-      bits::fa(c2[6], c2[7], c2[8], s2[2], c4[2]);
-      bits::fa(c2b[0], c2b[1], c2b[2], s2[3], c4[3]);
-      uint32_t s2b[2], c4b[2];
-      bits::fa(s2[0], s2[1], s2[2], s2b[0], c4b[0]);
-      bits::fa(s2[3], c2c, ONE, s2b[1], c4b[1]);  // +2 at weight 2
-      const uint32_t bit1 = s2b[0] ^ s2b[1];
-      const uint32_t c4c = s2b[0] & s2b[1];
-      uint32_t s4[2], c8[2];
-      bits::fa(c4[0], c4[1], c4[2], s4[0], c8[0]);
-      bits::fa(c4[3], c4b[0], c4b[1], s4[1], c8[1]);
-      uint32_t bit2, c8c;
-      bits::fa(s4[0], s4[1], c4c, bit2, c8c);
-      const uint32_t bit3 = ~(c8[0] ^ c8[1] ^ c8c);  // +8 at weight 8
-      // ---- back to bytes: byte b of V[r] = change + 8 of the voxel at bit 8b + r
-      // (0 for voxels this lane does not emit)
-      const uint32_t vm = rg.vmask;
-      uint32_t V[8] = {bit0 & vm, bit1 & vm, bit2 & vm, bit3 & vm, 0u, 0u, 0u, 0u};
-      bits::transpose8(V);
-      // ---- histogram: word += (change + 8) + 2^16 * emitted, at bin = value.
-      // PRMT builds [V.b, 0, vc.b, 0] (sign-replicating the < 128 bytes for 0).
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int p = 8 * b + r;
-          if (p >= 1 && p <= 30) {
-            const uint32_t bin = __byte_perm(P.wv[r], 0, 0x4440 + b);
-            const uint32_t inc =
-                bits::prmt(V[r], rg.vc[r], ((0xC + b) << 12) | ((4 + b) << 8) | ((0x8 + b) << 4) | b);
-            if constexpr (CH) {
-              if ((vm >> p) & 1) {
-                const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + rg.z0 + p;
-                g.chg[vox] = (int8_t)((int)((V[r] >> (8 * b)) & 0xFF) - 8);
-              }
-            } else {
-              atomicAdd(myhist + bin, inc);
-            }
+      for (int p = 1; p <= 30; ++p) {
+        const int r = p & 7, b = p >> 3;
+        const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
+                                        (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
+        if constexpr (CH) {
+          if ((vm >> p) & 1) {
+            const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + (cc.zs - 1) + p;
+            g.chg[vox] = (int8_t)decode_change(idx >> 8);
           }
+        } else {
+          // address = hist + 4 * idx on the FMA pipe (IMAD) rather than an
+          // ALU-pipe LEA: the integer ALU pipe is this kernel's bottleneck
+          uint32_t addr;
+          asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(idx), "r"(g.four), "r"(hist_s));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
         }
-      }
-      if (++since_flush == FLUSH_EVERY) {
-        since_flush = 0;
-        __syncwarp();
-        uint4* h4 = reinterpret_cast<uint4*>(myhist);
-        const uint4 h0 = h4[2 * lane], h1 = h4[2 * lane + 1];
-        const uint32_t hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t cnt = hv[j] >> 16;
-          accC[j] += cnt;
-          accS[j] += (int)(hv[j] & 0xFFFFu) - 8 * (int)cnt;
-        }
-        h4[2 * lane] = make_uint4(0, 0, 0, 0);
-        h4[2 * lane + 1] = make_uint4(0, 0, 0, 0);
-        __syncwarp();
       }
     }
-    xc.bx = bx;
-    xc.bxz = bxz;
-    xc.bxy = bxy;
-    xc.b8 = b8;
-    xc.bxyu = bxyu;
-    xc.b8u = b8u;
+    xc.gxa = gxa; xc.gxz = gxz; xc.gxz1 = gxz1; xc.gxy = gxy; xc.gxyu = gxyu;
+    xc.g8 = g8; xc.g81 = g81; xc.g8u = g8u; xc.g8u1 = g8u1;
   }
-  cc.next(g);
+  cc.next(g, nwt);
   ++step;
 }
 
 template <bool CH>
-__global__ void __launch_bounds__(NW * 32) k_u8_3d(const __grid_constant__ CUtensorMap map,
-                                                    Geom g, int64_t* __restrict__ ghist) {
+__global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
+    k_u8_3d(const __grid_constant__ CUtensorMap map, Geom g, int64_t* __restrict__ ghist) {
   extern __shared__ __align__(128) uint8_t dsm[];
-  auto ring = reinterpret_cast<uint8_t(*)[NS][STAGE]>(dsm);                 // [NW][NS][STAGE]
-  auto full = reinterpret_cast<uint64_t(*)[NS]>(dsm + RING_BYTES);          // [NW][NS]
-  auto hist = reinterpret_cast<uint32_t(*)[256]>(dsm + RING_BYTES + BAR_BYTES);  // [NW][256]
-  auto red = reinterpret_cast<long long(*)[512]>(dsm);  // aliases the ring after the sweep
+  auto ring = reinterpret_cast<uint8_t(*)[NS][STAGE]>(dsm);              // [NW][NS][STAGE]
+  auto full = reinterpret_cast<uint64_t(*)[NS]>(dsm + RING_BYTES);       // [NW][NS]
+  uint32_t* hist = reinterpret_cast<uint32_t*>(dsm + RING_BYTES + BAR_BYTES);  // [NCODE][256]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const unsigned FULL = 0xFFFFFFFFu;
   uint8_t(*myring)[STAGE] = ring[warp];
   uint64_t* myfull = full[warp];
-  uint32_t* myhist = hist[warp];
 
+  if (!CH)
+    for (int i = threadIdx.x; i < HIST_WORDS; i += NW * 32) hist[i] = 0;
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&myfull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int b = lane; b < 256; b += 32) myhist[b] = 0;
-  __syncwarp();
+  __syncthreads();
 
-  const long long nwarps = (long long)gridDim.x * NW;
-  const long long gw = (long long)blockIdx.x * NW + warp;
-  const long long La = g.total * gw / nwarps, Lb = g.total * (gw + 1) / nwarps;
+  const int nwt = gridDim.x * NW;
+  const int gw = blockIdx.x * NW + warp;
 
-  // producer cursor (lane 0 issues, the whole warp tracks it)
   Cursor pc, cc;
-  pc.start(g, La, Lb);
-  cc.start(g, La, Lb);
+  pc.start(g, gw);
+  cc.start(g, gw);
   auto issue = [&](int slot) {
-    const int X = g.own0 + pc.xo - 1 + pc.k;  // image plane
     if (lane == 0) {
+      const int X = pc.x0 - 1 + pc.k;  // image plane
       mbar_expect_tx(&myfull[slot], STAGE);
       // TMA needs the axis-2 box origin on a 16-byte boundary
       tma_load3(myring[slot], &map, ((pc.zs - 1) >> 4) << 4, pc.ys - 1, X - g.plane0, &myfull[slot]);
     }
-    pc.next(g);
+    pc.next(g, nwt);
   };
-  for (int s = 0; s < NS && pc.valid(); ++s) issue(s);
-
-  // per-lane accumulators for bins 8*lane .. 8*lane+7
-  int accS[8];
-  uint32_t accC[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) accS[j] = 0, accC[j] = 0;
+  for (int s = 0; s < NS && pc.valid(g); ++s) issue(s);
 
   Row A, B;
-  A.clear();
-  B.clear();
   XCarry xc;
   xc.clear();
   RunGeom rg;
-  int step = 0, since_flush = 0;
-  while (cc.valid()) {
-    if (cc.k == 0) rg.set(g, cc.col, lane);
+  int step = 0;
+  while (cc.valid(g)) {
+    if (cc.k == 0) rg.set(g, cc, lane);
     // unrolled by two so the carried row state ping-pongs without moves
-    sweep_step<CH>(g, cc, rg, step, since_flush, myring, myfull, myhist, pc, lane, A, B, xc, accS,
-               accC, issue);
-    if (!cc.valid()) break;
-    if (cc.k == 0) rg.set(g, cc.col, lane);
-    sweep_step<CH>(g, cc, rg, step, since_flush, myring, myfull, myhist, pc, lane, B, A, xc, accS,
-               accC, issue);
+    sweep_step<CH>(g, cc, rg, step, myring, myfull, hist, pc, nwt, lane, A, B, xc, issue);
+    if (!cc.valid(g)) break;
+    if (cc.k == 0) rg.set(g, cc, lane);
+    sweep_step<CH>(g, cc, rg, step, myring, myfull, hist, pc, nwt, lane, B, A, xc, issue);
   }
-  // drain the warp histogram
-  __syncwarp();
-  {
-    const uint4 h0 = reinterpret_cast<const uint4*>(myhist)[2 * lane];
-    const uint4 h1 = reinterpret_cast<const uint4*>(myhist)[2 * lane + 1];
-    const uint32_t hv[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+  if constexpr (!CH) {
+    __syncthreads();
+    // per value: change sum and voxel count over the codes (8 = not emitted)
+    for (int v = threadIdx.x; v < 256; v += NW * 32) {
+      long long sum = 0, cnt = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint32_t cnt = hv[j] >> 16;
-      accC[j] += cnt;
-      accS[j] += (int)(hv[j] & 0xFFFFu) - 8 * (int)cnt;
+      for (int c = 0; c < NCODE; ++c) {
+        if (c == 8) continue;
+        const long long n = hist[c * 256 + v];
+        cnt += n;
+        sum += n * decode_change((uint32_t)c);
+      }
+      if (cnt != 0) {
+        if (sum != 0)
+          atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[v]),
+                    static_cast<unsigned long long>(sum));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[256 + v]),
+                  static_cast<unsigned long long>(cnt));
+      }
     }
-  }
-  __syncthreads();  // every warp is past its sweep: the ring is free
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    red[warp][8 * lane + j] = accS[j];
-    red[warp][256 + 8 * lane + j] = accC[j];
-  }
-  __syncthreads();
-  for (int b = threadIdx.x; b < 512; b += NW * 32) {
-    long long s = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w][b];
-    if (s != 0)
-      atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[b]), static_cast<unsigned long long>(s));
   }
 }
 
@@ -490,10 +417,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 // Shape gate for the fast path: 3D, axis-2 rows a multiple of 16 bytes (TMA
-// stride rule), 16-byte aligned slab base.
+// stride rule), 16-byte aligned slab base, and per-CTA voxel counts that fit
+// the 32-bit shared counters.
 bool u8_3d_supported(const Slab& s) {
   return s.w2 > 1 && s.w2 % 16 == 0 && (reinterpret_cast<uintptr_t>(s.base) % 16) == 0 &&
-         s.w1 <= (1 << 30) && s.w2 <= (1 << 30) && s.w0 <= (1 << 30);
+         s.w1 <= (1 << 30) && s.w2 <= (1 << 30) && s.w0 <= (1 << 30) &&
+         (s.own1 - s.own0) * s.w1 * s.w2 < (1ll << 40);
 }
 
 cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st) {
@@ -518,10 +447,9 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.P = (int)(s.own1 - s.own0);
   g.Gy = (g.W1 + 29) / 30;
   g.Gz = (g.W2 + 29) / 30;
-  g.total = (long long)g.Gy * g.Gz * g.P;
+  g.ncols = g.Gy * g.Gz;
   g.chg = chg;
-  g.dbg = nullptr;
-  if (const char* e = getenv("ECC_DBG_PTR")) g.dbg = reinterpret_cast<uint32_t*>(strtoull(e, nullptr, 0));
+  g.four = 4;
   static int per_sm = -1;
   if (per_sm < 0) {
     cudaFuncSetAttribute(k_u8_3d<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
@@ -531,9 +459,21 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
         per_sm < 1)
       per_sm = 1;
   }
-  // enough warps that each sweeps >= ~64 planes, at most one full wave
-  long long want = (g.total / 64 + NW - 1) / NW;
-  long long grid = std::min<long long>((long long)sms * per_sm, std::max<long long>(1, want));
+  const long long cap_warps = (long long)sms * per_sm * NW;
+  // Segments along axis 0: one wave of (segment, column) units when the
+  // columns alone under-fill the GPU, else ~8 units per resident warp.
+  long long nseg;
+  if (g.ncols <= cap_warps)
+    nseg = std::max<long long>(1, cap_warps / g.ncols);
+  else
+    nseg = (8 * cap_warps + g.ncols - 1) / g.ncols;
+  nseg = std::min<long long>(nseg, std::max(1, g.P / 8));  // segments of >= 8 planes
+  g.seglen = (int)((g.P + nseg - 1) / nseg);
+  nseg = (g.P + g.seglen - 1) / g.seglen;
+  const long long units = nseg * g.ncols;
+  if (units > (1ll << 30)) return cudaErrorInvalidValue;
+  g.nunits = (int)units;
+  const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
   if (chg)
     k_u8_3d<true><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
   else

@@ -1,0 +1,56 @@
+// CPU check of the bit-sliced carry-save sum used by k_u8_3d.cu
+// (bits::sum_code): random masks, every lane-bit compared with a scalar sum.
+// Built and run by tests/test_native_cpu.py.
+#include <cstdint>
+#include <cstdio>
+#include <random>
+
+#define __host__
+#define __device__
+#define __forceinline__ inline
+#include "../../paper_2203_09087_b200/csrc/bits.cuh"
+
+int main() {
+  std::mt19937 rng(7);
+  for (int it = 0; it < 20000; ++it) {
+    uint32_t w1[17], w2[9], out[4];
+    const int bias = it % 5;  // vary densities
+    for (auto& x : w1) x = bias == 0 ? rng() : (bias == 1 ? rng() & rng() : (bias == 2 ? rng() | rng() : (bias == 3 ? 0xFFFFFFFFu : 0u)));
+    for (auto& x : w2) x = bias == 4 ? rng() : (bias == 3 ? rng() | rng() : rng() & rng());
+    eccb::bits::sum_code(w1, w2, out);
+    for (int p = 0; p < 32; ++p) {
+      int s = 0;
+      for (auto x : w1) s += (x >> p) & 1;
+      for (auto x : w2) s += 2 * ((x >> p) & 1);
+      int got = 0;
+      for (int k = 0; k < 4; ++k) got |= ((out[k] >> p) & 1) << k;
+      if (got != (s & 15)) {
+        std::printf("mismatch it=%d p=%d want %d got %d\n", it, p, s & 15, got);
+        return 1;
+      }
+    }
+  }
+  std::printf("sum_code ok\n");
+  return 0;
+}
+// (appended) transpose_codes == transpose8 on {p0..p3, 0, 0, 0, 0}
+int test_transpose_codes() {
+  std::mt19937 rng(11);
+  for (int it = 0; it < 20000; ++it) {
+    uint32_t p[4] = {(uint32_t)rng(), (uint32_t)rng(), (uint32_t)rng(), (uint32_t)rng()};
+    uint32_t a[8] = {p[0], p[1], p[2], p[3], 0, 0, 0, 0}, b[8];
+    eccb::bits::transpose8(a);
+    eccb::bits::transpose_codes(p[0], p[1], p[2], p[3], b);
+    for (int r = 0; r < 8; ++r)
+      if (a[r] != b[r]) { std::printf("transpose_codes mismatch\n"); return 1; }
+    // and the meaning: byte b of w[r] = code of lane-bit 8b + r
+    for (int q = 0; q < 32; ++q) {
+      int want = 0;
+      for (int k = 0; k < 4; ++k) want |= ((p[k] >> q) & 1) << k;
+      if ((int)((b[q & 7] >> (8 * (q >> 3))) & 0xFF) != want) { std::printf("code layout mismatch\n"); return 1; }
+    }
+  }
+  std::printf("transpose_codes ok\n");
+  return 0;
+}
+static int run_extra = [] { return test_transpose_codes(); }();

@@ -166,8 +166,8 @@ void run_op(uint32_t* out, int sms, double ghz) {
 template <int V>
 void run_hist(uint32_t* out, int sms, double ghz, const char* name) {
   const int threads = 512, blocks = sms * 2;
-  const size_t smem = (V == 3) ? 256 * 32 * 16 * 4 / 2 : 4096 * 4;
-  const int thr = (V == 3) ? 256 : threads;
+  const size_t smem = (V == 3) ? 256 * 32 * 8 * 4 / 2 : 4096 * 4;
+  const int thr = (V == 3) ? 128 : threads;
   CK(cudaFuncSetAttribute(k_hist<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const double upd = double(blocks) * thr * HI;
   float ms = time_ms([&] { k_hist<V><<<blocks, thr, smem>>>(out, 7); });
