@@ -193,14 +193,18 @@ __device__ __forceinline__ int decode_change(uint32_t code) {
   return code >= 10 ? (int)code - 17 : (int)code - 1;
 }
 
-template <bool CH, class Issue>
-__device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunGeom& rg, int& step,
+// One plane step of a column: plane X arrives as row N, row P holds plane
+// X-1.  KIND 0: the unit's first (halo) plane, tournament only; KIND 1: +
+// x comparisons against P (P may be the x = -1 collar); KIND 2: + the
+// changes of P (X-1 is an owned plane).
+template <bool CH, int KIND, class Issue>
+__device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int zs,
+                                           const RunGeom& rg, int& step,
                                            uint8_t (*myring)[STAGE], uint64_t* myfull,
-                                           uint32_t* hist, const Cursor& pc, int nwt, int lane,
+                                           uint32_t* hist, const Cursor& pc, int lane,
                                            Row& P, Row& N, XCarry& xc, Issue& issue) {
-  const int slot = step % NS;
+  const int slot = step & (NS - 1);
   const uint32_t phase = (uint32_t)((step / NS) & 1);
-  const int X = cc.x0 - 1 + cc.k;
   mbar_wait(&myfull[slot], phase);
   {
     const uint4* rowp = reinterpret_cast<const uint4*>(myring[slot] + lane * BOXZ);
@@ -228,7 +232,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunG
   bits::byte_interleave(N.W, C);
   bits::transpose8(C);
   // collar: voxels outside the image hold 255 (TMA filled zeros)
-  const bool xout = (X < 0) | (X >= g.W0);
+  const bool xout = (KIND == 0 ? X < 0 : false) | (X >= g.W0);
   if (rg.edge | xout) {  // warp-uniform: only columns / planes touching the collar
     const uint32_t om = (rg.yout | xout) ? FULL : rg.zout;
 #pragma unroll
@@ -258,18 +262,18 @@ __device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunG
     N.gyz = gyz;
   }
 
-  if (cc.k >= 1) {
+  if constexpr (KIND >= 1) {
     // ---- x comparisons between planes X-1 (P) and X (N): "X wins" bits
     uint32_t gxa = bits::gt<8>(P.C, N.C);
     uint32_t gxz = bits::gt<8>(P.mz, N.mz);
     uint32_t gxy = bits::gt<8>(P.my, N.my);
     uint32_t g8 = bits::gt<8>(P.myz, N.myz);
-    if (X - 1 < 0) gxa = gxz = gxy = g8 = FULL;  // x = -1 never wins
+    if (KIND == 1 && X - 1 < 0) gxa = gxz = gxy = g8 = FULL;  // x = -1 never wins
     const uint32_t gxz1 = gxz << 1, g81 = g8 << 1;
     const uint32_t gxyu = __shfl_up_sync(FULL, gxy, 1);
     const uint32_t g8u = __shfl_up_sync(FULL, g8, 1);
     const uint32_t g8u1 = g8u << 1;
-    if (cc.k >= 2) {
+    if constexpr (KIND == 2) {
       // ---- changes of row X-1: each voxel gathers its 26 block wins
       const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
       const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
@@ -307,7 +311,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunG
                                         (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
         if constexpr (CH) {
           if ((vm >> p) & 1) {
-            const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + (cc.zs - 1) + p;
+            const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + (zs - 1) + p;
             g.chg[vox] = (int8_t)decode_change(idx >> 8);
           }
         } else {
@@ -322,7 +326,6 @@ __device__ __forceinline__ void sweep_step(const Geom& g, Cursor& cc, const RunG
     xc.gxa = gxa; xc.gxz = gxz; xc.gxz1 = gxz1; xc.gxy = gxy; xc.gxyu = gxyu;
     xc.g8 = g8; xc.g81 = g81; xc.g8u = g8u; xc.g8u1 = g8u1;
   }
-  cc.next(g, nwt);
   ++step;
 }
 
@@ -349,9 +352,8 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
   const int nwt = gridDim.x * NW;
   const int gw = blockIdx.x * NW + warp;
 
-  Cursor pc, cc;
+  Cursor pc;
   pc.start(g, gw);
-  cc.start(g, gw);
   auto issue = [&](int slot) {
     if (lane == 0) {
       const int X = pc.x0 - 1 + pc.k;  // image plane
@@ -365,16 +367,23 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
 
   Row A, B;
   XCarry xc;
-  xc.clear();
   RunGeom rg;
   int step = 0;
-  while (cc.valid(g)) {
-    if (cc.k == 0) rg.set(g, cc, lane);
-    // unrolled by two so the carried row state ping-pongs without moves
-    sweep_step<CH>(g, cc, rg, step, myring, myfull, hist, pc, nwt, lane, A, B, xc, issue);
-    if (!cc.valid(g)) break;
-    if (cc.k == 0) rg.set(g, cc, lane);
-    sweep_step<CH>(g, cc, rg, step, myring, myfull, hist, pc, nwt, lane, B, A, xc, issue);
+  for (int u = gw; u < g.nunits; u += nwt) {
+    Cursor cc;
+    cc.start(g, u);
+    rg.set(g, cc, lane);
+    const int x0 = cc.x0, zs = cc.zs, len = cc.len;
+    sweep_step<CH, 0>(g, x0 - 1, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
+    sweep_step<CH, 1>(g, x0, zs, rg, step, myring, myfull, hist, pc, lane, A, B, xc, issue);
+    // planes x0+1 .. x0+len: the changes of x0 .. x0+len-1
+    int X = x0 + 1;
+    for (; X + 1 <= x0 + len; X += 2) {
+      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
+      sweep_step<CH, 2>(g, X + 1, zs, rg, step, myring, myfull, hist, pc, lane, A, B, xc, issue);
+    }
+    if (X <= x0 + len)
+      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
   }
   if constexpr (!CH) {
     __syncthreads();
