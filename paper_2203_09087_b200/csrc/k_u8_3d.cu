@@ -65,7 +65,7 @@ constexpr int HIST_WORDS = NCODE * 256;
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + HIST_WORDS * 4;
-constexpr int CTAS_PER_SM = 3;
+constexpr int CTAS_PER_SM = 4;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
 struct Geom {
