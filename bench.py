@@ -3,10 +3,11 @@
 Workload (config 2 of BASELINE.json, the one the metric is quoted on): each
 rank owns a 512^3 u8 z-slab (axis-0 planes [512 r, 512 r + 512)) of a
 (512 N) x 512 x 512 synthetic volume (v = counter_hash(1,
-i) >> 56), plus one halo plane from each neighbouring slab.  One step =
-K1+K2 (stencil + histogram) over the slab, one NCCL all-reduce of the
-2 x 256 int64 histogram when N > 1, and K3 (compaction + prefix sum).  Per-GPU
-work is fixed as N grows ("scaling": "weak").
+i) >> 56), plus one halo plane from each neighbouring slab.  One step at
+N = 1 is ONE fused launch (ecc_curve_device: stencil + histogram + the last
+CTA's compaction + prefix sum); at N > 1 it is K1+K2 over the slab, one NCCL
+all-reduce of the 2 x 256 int64 histogram, and K3.  Per-GPU work is fixed as
+N grows ("scaling": "weak").
 
 * value     -- device-resident voxels/s (inputs already in HBM), CUDA events
                on the compute stream, max over ranks, L2 flushed (256 MiB
@@ -15,8 +16,9 @@ work is fixed as N grows ("scaling": "weak").
                buffer (ecc_curve for N = 1; per-rank H2D + slab + all-reduce +
                finalize + D2H for N > 1), host<->device copies inside the
                timed region.
-* roofline  -- K1+K2 alone: algorithmic bytes (1 B/voxel read) / kernel
-               time vs MEASURED_PEAKS.json hbm_gbs.
+* roofline  -- the dominant kernel (k_u8_3d: K1+K2, with K3 fused at N = 1):
+               algorithmic bytes (1 B/voxel read) / its CUDA-event time vs
+               MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline -- the reference engine (oracle/_ref, compiled from the
                reference sources) on this host's cores, rank 0 at N = 1.
 
@@ -52,7 +54,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled through NVML every 20 ms while
+    """SM clocks + throttle reasons sampled through NVML every 5 ms while
     the timed region runs (the recipe's nvidia-smi clocks line, in-process)."""
 
     def __init__(self, index: int):
@@ -89,7 +91,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            self._stop.wait(0.02)
+            self._stop.wait(0.005)
 
     def __exit__(self, *a):
         self._stop.set()
@@ -134,7 +136,7 @@ def cpu_reference_run(steps: int, warmup: int, budget_s: float):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -194,14 +196,21 @@ def main():
 
     def step(ev_k0=None, ev_k1=None):
         with torch.cuda.stream(stream):
+            if dist is None:
+                # whole volume on one GPU: ONE fused launch (K1+K2+K3)
+                if ev_k0 is not None:
+                    ev_k0.record(stream)
+                ctx.curve_device(slab, dims, bins, chg, chi, cnt, stream=ctx.stream)
+                if ev_k1 is not None:
+                    ev_k1.record(stream)
+                return
             hist.zero_()
             if ev_k0 is not None:
                 ev_k0.record(stream)
             ctx.accumulate_slab(slab, dims, p0, own0, own1, hist, stream=ctx.stream)
             if ev_k1 is not None:
                 ev_k1.record(stream)
-            if dist is not None:
-                dist.all_reduce(hist)
+            dist.all_reduce(hist)
             ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
 
     # correctness of what we time: final chi of a complete volume is 1
@@ -215,21 +224,26 @@ def main():
     torch.cuda.synchronize()
     l0 = ctx.launch_count()
     step_ms, kern_ms = [], []
+    # K steps enqueued back to back (the host runs ahead, so launch latency is
+    # hidden behind the previous step's L2 flush); each step is bracketed by
+    # CUDA events on the compute stream, the whole region by barrier + sync.
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            a, b, k0, k1 = evs[i]
             with torch.cuda.stream(stream):
                 flush.fill_(1)  # evict L2 (126 MB) between timed steps
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if dist is not None:
-                dist.barrier()
-            torch.cuda.synchronize()
             a.record(stream)
             step(k0, k1)
             b.record(stream)
-            torch.cuda.synchronize()
-            step_ms.append(a.elapsed_time(b))
-            kern_ms.append(k0.elapsed_time(k1))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b, _, _ in evs]
+    kern_ms = [k0.elapsed_time(k1) for _, _, k0, k1 in evs]
     launches = ctx.launch_count() - l0
     t_step = sum(step_ms) / len(step_ms)
     t_kern = sum(kern_ms) / len(kern_ms)

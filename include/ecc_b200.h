@@ -138,6 +138,18 @@ ECC_API int ecc_finalize(ecc_ctx* ctx, const int64_t* d_hist, uint64_t nbins,
                  uint32_t* d_bins, int64_t* d_changes, int64_t* d_chi,
                  uint64_t* d_count, void* stream);
 
+/* Device-resident whole image -> curve in device buffers: process_image
+ * (streaming.hpp:332-338) + vcec_to_ecc (curve.hpp:28-35) for an image that
+ * is already in HBM.  3D u8 volumes whose rows are a multiple of 16 bytes
+ * take ONE fused launch (stencil + histogram + compaction + prefix sum in
+ * the last CTA); other shapes take memset + K1/K2 + K3.  d_bins (uint32),
+ * d_changes / d_chi (int64) have capacity ecc_bin_count(); *d_count (device
+ * uint64) receives the number of occurring values.  Not valid for
+ * ECC_BIN_SORTED.  One call in flight per context. */
+ECC_API int ecc_curve_device(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
+                     const ecc_binmap* bm, uint32_t* d_bins, int64_t* d_changes,
+                     int64_t* d_chi, uint64_t* d_count, void* stream);
+
 /* ------------------------------------------------------------ L4: whole images
  * process_image(const Image<T>&, plan) (streaming.hpp:332-338) + the VCEC
  * result.  `data` is host (where = 0) or device (where = 1).  Outputs are

@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
             L.ecc_accumulate_slab.argtypes = slab + [C.POINTER(_BinMap), _vp, _vp]
             L.ecc_compute_changes.argtypes = slab + [_vp, _vp]
             L.ecc_finalize.argtypes = [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]
+            L.ecc_curve_device.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp,
+                                           _vp, _vp, _vp]
             vol = [_vp, _vp, C.c_int, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp, _u64, C.POINTER(_u64)]
             L.ecc_vcec.argtypes = vol
             L.ecc_curve.argtypes = vol
@@ -108,7 +110,7 @@ def lib() -> C.CDLL:
             L.ecc_fill_synthetic.argtypes = [_vp, _vp, C.c_int, _u64, _u64, _u64, _vp]
             for n in ("ecc_ctx_create", "ecc_bin_count", "ecc_accumulate_slab", "ecc_compute_changes",
                       "ecc_finalize", "ecc_vcec", "ecc_curve", "ecc_process_stream", "ecc_batch2d",
-                      "ecc_fill_synthetic"):
+                      "ecc_fill_synthetic", "ecc_curve_device"):
                 getattr(L, n).restype = C.c_int
             _lib = L
         return _lib
@@ -489,6 +491,17 @@ class Context:
         _check(lib().ecc_compute_changes(self._p, planes.data_ptr(), dt,
                                          _Dims(dims.w0, dims.w1, dims.w2), plane0, nplanes, own0,
                                          own1, out.data_ptr(), stream or None))
+
+    def curve_device(self, image, dims: Dims, bins, changes, chi, count, binmap=None,
+                     stream: int = 0):
+        """Device-resident image -> curve in device tensors (ecc_curve_device):
+        one fused launch for 3D u8 volumes."""
+        import torch
+        dt = {torch.uint8: ECC_U8, torch.uint16: ECC_U16, torch.float32: ECC_F32}[image.dtype]
+        bm = _binmap(dt, binmap)
+        _check(lib().ecc_curve_device(self._p, image.data_ptr(), dt, _Dims(dims.w0, dims.w1, dims.w2),
+                                      C.byref(bm), bins.data_ptr(), changes.data_ptr(),
+                                      chi.data_ptr(), count.data_ptr(), stream or None))
 
     def finalize(self, hist, nbins: int, bins, changes, chi, count, stream: int = 0):
         _check(lib().ecc_finalize(self._p, hist.data_ptr(), nbins, bins.data_ptr(),

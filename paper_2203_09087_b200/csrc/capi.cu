@@ -126,6 +126,7 @@ struct ecc_ctx {
   DevBuf slab[2];
   PinBuf staging[2];
   PinBuf host_small;
+  DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
 };
 
 namespace {
@@ -243,6 +244,40 @@ struct BinResult {
   std::vector<int64_t> changes;
   std::vector<int64_t> chi;
 };
+
+// Whole 3D u8 image in ONE launch (k_u8_3d with the fused last-CTA K3).
+bool fusable(ecc_dtype dtype, const Slab& s, bool affine) {
+  return dtype == ECC_U8 && !affine && u8_3d_supported(s);
+}
+
+int launch_fused(ecc_ctx* ctx, const Slab& s, uint32_t* bins, int64_t* changes, int64_t* chi,
+                 uint64_t* count, cudaStream_t st) {
+  if (!ctx->fused.p) {
+    CKI(ctx->fused.ensure(256 + 512 * 8));
+    CKR(cudaMemsetAsync(ctx->fused.p, 0, 256 + 512 * 8, st));
+  }
+  U83dFinalize fz{ctx->fused.as<uint32_t>(), bins, changes, chi, count};
+  CKR(launch_u8_3d(s, reinterpret_cast<int64_t*>(ctx->fused.as<uint8_t>() + 256), nullptr,
+                   ctx->sms, st, &fz));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+int copy_result_to_host(ecc_ctx* ctx, cudaStream_t st, BinResult* out) {
+  uint64_t m = 0;
+  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  out->bins.resize(m);
+  out->changes.resize(m);
+  out->chi.resize(m);
+  if (m) {
+    CKR(cudaMemcpyAsync(out->bins.data(), ctx->bins.p, m * 4, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->changes.data(), ctx->changes.p, m * 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->chi.data(), ctx->chi.p, m * 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+  }
+  return ECC_OK;
+}
 
 int finalize_to_host(ecc_ctx* ctx, uint32_t nbins, cudaStream_t st, BinResult* out) {
   CKI(ctx->bins.ensure(nbins * 4ull));
@@ -390,6 +425,15 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
     merge_runs(keys, sums, {0, keys.size()}, res);
     return ECC_OK;
   }
+  if (fusable(dtype, s, affine)) {
+    CKI(ctx->bins.ensure(nbins * 4ull));
+    CKI(ctx->changes.ensure(nbins * 8ull));
+    CKI(ctx->chi.ensure(nbins * 8ull));
+    CKI(ctx->count.ensure(8));
+    CKI(launch_fused(ctx, s, ctx->bins.as<uint32_t>(), ctx->changes.as<int64_t>(),
+                     ctx->chi.as<int64_t>(), ctx->count.as<uint64_t>(), st));
+    return copy_result_to_host(ctx, st, res);
+  }
   CKI(ctx->hist.ensure(2 * nbins * 8));
   CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
   CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
@@ -449,7 +493,7 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   cudaStreamSynchronize(ctx->copy);
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
-                    &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1]})
+                    &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->fused})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -504,6 +548,34 @@ int ecc_compute_changes(ecc_ctx* ctx, const void* d_planes, ecc_dtype dtype,
   CKR(launch_changes_fast(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream), &handled));
   if (!handled) CKR(launch_generic_changes(s, (int)dtype, d_out, ctx->sms, pick(ctx, stream)));
   ctx->launches += 1;
+  return ECC_OK;
+}
+
+int ecc_curve_device(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
+                     const ecc_binmap* bm, uint32_t* d_bins, int64_t* d_changes, int64_t* d_chi,
+                     uint64_t* d_count, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_dims(dims));
+  if (!d_data || !d_bins || !d_changes || !d_chi || !d_count)
+    return fail(ECC_EINVAL, "null device pointer");
+  uint64_t nbins;
+  bool affine, sorted;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  if (sorted) return fail(ECC_EINVAL, "the sorted bin map has no device-side curve; use ecc_curve");
+  cudaStream_t st = pick(ctx, stream);
+  const Slab s = make_slab(d_data, dims, 0, dims.w0, 0, dims.w0);
+  if (fusable(dtype, s, affine)) return launch_fused(ctx, s, d_bins, d_changes, d_chi, d_count, st);
+  CKI(ctx->flags.ensure(4));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  CKI(ctx->hist.ensure(2 * nbins * 8));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
+  CKR(launch_finalize(ctx->hist.as<int64_t>(), (uint32_t)nbins, d_bins, d_changes, d_chi, d_count,
+                      st));
+  ctx->launches += 1;
+  if (affine) CKI(read_flags(ctx, st));
   return ECC_OK;
 }
 

@@ -9,6 +9,20 @@
 
 namespace eccb {
 
+// Workspace of the fused single-launch curve (k_u8_3d.cu): `ticket` and the
+// 512-entry int64 histogram must be zero before the launch and are zero
+// again after it.
+struct U83dFinalize {
+  uint32_t* ticket;
+  uint32_t* bins;
+  int64_t* changes;
+  int64_t* chi;
+  uint64_t* count;
+};
+bool u8_3d_supported(const Slab& s);
+cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st,
+                         const U83dFinalize* fz = nullptr);
+
 cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
                                       const AffineMap& am, int64_t* ghist,
                                       uint32_t nbins, uint32_t* flags, int sms,

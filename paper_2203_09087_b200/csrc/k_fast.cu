@@ -4,8 +4,6 @@
 
 namespace eccb {
 
-bool u8_3d_supported(const Slab& s);
-cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st);
 
 cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
                                    const AffineMap& am, int64_t* ghist,

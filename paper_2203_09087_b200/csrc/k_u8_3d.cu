@@ -48,6 +48,8 @@
 #include <algorithm>
 #include <cstdint>
 
+#include <cub/cub.cuh>
+
 #include "bits.cuh"
 #include "ecc_common.cuh"
 #include "internal.h"
@@ -79,6 +81,17 @@ struct Geom {
   int nunits;      // ncols * segments
   int8_t* chg;     // CH mode: per-voxel changes of the owned planes (compute_changes)
   uint32_t four;   // = 4, opaque to ptxas so the histogram address stays an IMAD
+};
+
+// Fused K3 (optional): the last CTA to finish turns the global histogram
+// into the curve (merge_local + vcec_to_ecc, vcec.hpp:35-66, curve.hpp:28-35)
+// and re-zeroes the histogram and the ticket for the next launch.
+struct Fin {
+  uint32_t* ticket;    // zero before the launch, zero again after it
+  uint32_t* bins;      // [256] occurring values, ascending
+  int64_t* changes;    // [256] their VCEC entries
+  int64_t* chi;        // [256] the curve
+  uint64_t* count;     // number of occurring values
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -331,7 +344,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
 
 template <bool CH>
 __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
-    k_u8_3d(const __grid_constant__ CUtensorMap map, Geom g, int64_t* __restrict__ ghist) {
+    k_u8_3d(const __grid_constant__ CUtensorMap map, Geom g, int64_t* __restrict__ ghist, Fin fin) {
   extern __shared__ __align__(128) uint8_t dsm[];
   auto ring = reinterpret_cast<uint8_t(*)[NS][STAGE]>(dsm);              // [NW][NS][STAGE]
   auto full = reinterpret_cast<uint64_t(*)[NS]>(dsm + RING_BYTES);       // [NW][NS]
@@ -405,6 +418,41 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
                   static_cast<unsigned long long>(cnt));
       }
     }
+    if (fin.ticket) {
+      __shared__ bool last;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) last = atomicAdd(fin.ticket, 1u) == gridDim.x - 1;
+      __syncthreads();
+      if (last) {
+        __threadfence();
+        // thread t owns values 2t, 2t+1
+        using Scan = cub::BlockScan<longlong2, NW * 32>;
+        __shared__ typename Scan::TempStorage tmp;
+        const int v0 = 2 * threadIdx.x;
+        const long long s0 = __ldcg(&ghist[v0]), s1 = __ldcg(&ghist[v0 + 1]);
+        const long long n0 = __ldcg(&ghist[256 + v0]), n1 = __ldcg(&ghist[256 + v0 + 1]);
+        longlong2 in = make_longlong2((n0 != 0) + (n1 != 0), s0 + s1), ex, total;
+        struct Add {
+          __device__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+            return make_longlong2(a.x + b.x, a.y + b.y);
+          }
+        };
+        Scan(tmp).ExclusiveScan(in, ex, make_longlong2(0, 0), Add(), total);
+        long long pos = ex.x, acc = ex.y;
+        acc += s0;
+        if (n0 != 0) {
+          fin.bins[pos] = v0; fin.changes[pos] = s0; fin.chi[pos] = acc; ++pos;
+        }
+        acc += s1;
+        if (n1 != 0) {
+          fin.bins[pos] = v0 + 1; fin.changes[pos] = s1; fin.chi[pos] = acc;
+        }
+        if (threadIdx.x == 0) *fin.count = (uint64_t)total.x;
+        ghist[v0] = 0; ghist[v0 + 1] = 0; ghist[256 + v0] = 0; ghist[256 + v0 + 1] = 0;
+        if (threadIdx.x == 0) *fin.ticket = 0;
+      }
+    }
   }
 }
 
@@ -434,19 +482,36 @@ bool u8_3d_supported(const Slab& s) {
          (s.own1 - s.own0) * s.w1 * s.w2 < (1ll << 40);
 }
 
-cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st) {
+cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st,
+                         const U83dFinalize* fz) {
   using namespace u83d;
-  auto enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
-  CUtensorMap map;
-  const cuuint64_t dims[3] = {(cuuint64_t)s.w2, (cuuint64_t)s.w1, (cuuint64_t)s.nplanes};
-  const cuuint64_t strides[2] = {(cuuint64_t)s.w2, (cuuint64_t)(s.w1 * s.w2)};
-  const cuuint32_t box[3] = {BOXZ, BOXY, 1};
-  const cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(s.base), dims, strides,
-                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  // the tensor map of the last slab is cached per host thread (encoding it
+  // is host work on every call otherwise)
+  thread_local struct {
+    const void* base = nullptr;
+    int64_t w1 = 0, w2 = 0, np = 0;
+    CUtensorMap map;
+  } cache;
+  if (cache.base != s.base || cache.w1 != s.w1 || cache.w2 != s.w2 || cache.np != s.nplanes) {
+    auto enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    const cuuint64_t dims[3] = {(cuuint64_t)s.w2, (cuuint64_t)s.w1, (cuuint64_t)s.nplanes};
+    const cuuint64_t strides[2] = {(cuuint64_t)s.w2, (cuuint64_t)(s.w1 * s.w2)};
+    const cuuint32_t box[3] = {BOXZ, BOXY, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&cache.map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(s.base), dims,
+                     strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      cache.base = nullptr;
+      return cudaErrorInvalidValue;
+    }
+    cache.base = s.base;
+    cache.w1 = s.w1;
+    cache.w2 = s.w2;
+    cache.np = s.nplanes;
+  }
+  const CUtensorMap& map = cache.map;
   Geom g;
   g.W0 = (int)s.w0;
   g.W1 = (int)s.w1;
@@ -483,10 +548,12 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
   const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
+  Fin fin{};
+  if (fz) fin = Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
   if (chg)
-    k_u8_3d<true><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
+    k_u8_3d<true><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist, fin);
   else
-    k_u8_3d<false><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
+    k_u8_3d<false><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist, fin);
   return cudaGetLastError();
 }
 
