@@ -1,0 +1,339 @@
+// C++ tests of the drop-in API (include/ecc/*.hpp) against the oracle's C
+// restatement, written like the reference's own unit tests
+// (proj/tests/test_streaming.cpp, test_kernel.cpp, acceptance.cpp).
+//
+//   test_api cpu   -- host-only cases (planning, validation, types)
+//   test_api gpu   -- GPU cases through libecc_b200.so (bit-exact parity)
+//
+// Built by tests/test_native_cpu.py / paper_2203_09087_b200/build.py.
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "ecc.hpp"
+
+extern "C" {
+// oracle/ecc_oracle.c (test infrastructure)
+int ecc_oracle_vcec_u8(const uint8_t*, uint64_t, uint64_t, uint64_t, int64_t*, int64_t*);
+int ecc_oracle_vcec_u16(const uint16_t*, uint64_t, uint64_t, uint64_t, int64_t*, int64_t*);
+int64_t ecc_oracle_vcec_f32(const float*, uint64_t, uint64_t, uint64_t, float*, int64_t*);
+void ecc_oracle_fill_u8(uint8_t*, uint64_t, uint64_t, uint64_t);
+}
+
+using namespace ecc;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                                   \
+  do {                                                                             \
+    ++g_checks;                                                                    \
+    if (!(c)) {                                                                    \
+      ++g_fail;                                                                    \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);           \
+    }                                                                              \
+  } while (0)
+#define CHECK_THROWS_WITH(expr, needle)                                            \
+  do {                                                                             \
+    ++g_checks;                                                                    \
+    bool thrown_ = false;                                                          \
+    try {                                                                          \
+      (void)(expr);                                                                \
+    } catch (const ecc::error& e_) {                                               \
+      thrown_ = std::string(e_.what()).find(needle) != std::string::npos;          \
+      if (!thrown_) std::printf("  message was: %s\n", e_.what());                  \
+    }                                                                              \
+    if (!thrown_) {                                                                \
+      ++g_fail;                                                                    \
+      std::printf("  CHECK_THROWS failed %s:%d: %s\n", __FILE__, __LINE__, #expr); \
+    }                                                                              \
+  } while (0)
+
+struct Case {
+  const char* name;
+  bool gpu;
+  std::function<void()> fn;
+};
+static std::vector<Case>& registry() {
+  static std::vector<Case> r;
+  return r;
+}
+struct Reg {
+  Reg(const char* n, bool g, std::function<void()> f) { registry().push_back({n, g, f}); }
+};
+#define CAT2(a, b) a##b
+#define CAT(a, b) CAT2(a, b)
+#define TEST_CPU(name) static Reg CAT(reg_, __LINE__)(name, false, []()
+#define TEST_GPU(name) static Reg CAT(reg_, __LINE__)(name, true, []()
+#define END_TEST );
+
+template <class T>
+static Image<T> image_2d(std::vector<std::vector<T>> rows) {
+  Image<T> img;
+  img.dims = {rows.size(), rows[0].size(), 1};
+  for (auto& r : rows) img.values.insert(img.values.end(), r.begin(), r.end());
+  return img;
+}
+
+template <class T>
+static GlobalVcec<T> run_engine(const Image<T>& img, std::uint64_t chunks = 1) {
+  return process_image(img, plan_chunks<T>(img.dims, ChunkTarget::count(chunks)));
+}
+
+template <class T>
+static GlobalVcec<T> oracle_vcec(const Image<T>& img) {
+  GlobalVcec<T> out;
+  const Dims& d = img.dims;
+  if constexpr (std::is_same_v<T, float>) {
+    std::vector<float> v(img.values.size());
+    std::vector<int64_t> c(img.values.size());
+    const int64_t m = ecc_oracle_vcec_f32(img.values.data(), d.w0, d.w1, d.w2, v.data(), c.data());
+    v.resize(m);
+    c.resize(m);
+    out.values = v;
+    out.changes = c;
+  } else {
+    const int nb = std::is_same_v<T, uint8_t> ? 256 : 65536;
+    std::vector<int64_t> h(nb), n(nb);
+    if constexpr (std::is_same_v<T, uint8_t>)
+      ecc_oracle_vcec_u8(img.values.data(), d.w0, d.w1, d.w2, h.data(), n.data());
+    else
+      ecc_oracle_vcec_u16(img.values.data(), d.w0, d.w1, d.w2, h.data(), n.data());
+    for (int b = 0; b < nb; ++b)
+      if (n[b]) {
+        out.values.push_back(static_cast<T>(b));
+        out.changes.push_back(h[b]);
+      }
+  }
+  return out;
+}
+
+template <class T>
+static bool same(const GlobalVcec<T>& a, const GlobalVcec<T>& b) {
+  if (a.values.size() != b.values.size() || a.changes != b.changes) return false;
+  return std::memcmp(a.values.data(), b.values.data(), a.values.size() * sizeof(T)) == 0;
+}
+
+// ------------------------------------------------------------------ host only
+TEST_CPU("plan_chunks splits with ceiling lengths") {  // test_streaming.cpp:13-19
+  const auto plan = plan_chunks<float>({10, 1, 1}, ChunkTarget::count(3));
+  CHECK(plan.ranges.size() == 3);
+  CHECK((plan.ranges[0] == ChunkRange{0, 4}));
+  CHECK((plan.ranges[1] == ChunkRange{4, 8}));
+  CHECK((plan.ranges[2] == ChunkRange{8, 10}));
+} END_TEST
+
+TEST_CPU("plan invariants hold for many (w0, c) pairs") {  // test_streaming.cpp:27-45
+  for (std::uint64_t w0 : {1, 2, 3, 7, 10, 64, 100})
+    for (std::uint64_t c : {1, 2, 3, 5, 8, 200}) {
+      const auto plan = plan_chunks<float>({w0, 4, 4}, ChunkTarget::count(c));
+      const std::uint64_t eff = std::min<std::uint64_t>(c, w0);
+      const std::uint64_t max_len = (w0 + eff - 1) / eff;
+      std::uint64_t b = 0;
+      for (const auto& r : plan.ranges) {
+        CHECK(r.begin == b);
+        CHECK(r.end > r.begin);
+        CHECK(r.len() <= max_len);
+        b = r.end;
+      }
+      CHECK(b == w0);
+    }
+} END_TEST
+
+TEST_CPU("budget-based planning keeps each padded chunk within budget") {
+  const Dims dims{4096, 512, 512};
+  const std::uint64_t budget = 64ull << 20;
+  const auto plan = plan_chunks<float>(dims, ChunkTarget::memory_budget(budget));
+  std::uint64_t max_len = 0;
+  for (const auto& r : plan.ranges) max_len = std::max(max_len, r.len());
+  CHECK(padded_chunk_bytes<float>(dims, max_len) <= budget);
+} END_TEST
+
+TEST_CPU("an infeasible budget names the minimum") {  // test_streaming.cpp:56-66
+  const Dims dims{8, 1024, 1024};
+  CHECK_THROWS_WITH(plan_chunks<float>(dims, ChunkTarget::memory_budget(1024)),
+                    std::to_string(2 * padded_chunk_bytes<float>(dims, 1)));
+} END_TEST
+
+TEST_CPU("linear_index names out-of-range coordinates") {
+  CHECK_THROWS_WITH(linear_index({3, 0, 0}, Dims{3, 2, 2}), "out of range for dims 3x2x2");
+  CHECK(linear_index({1, 1, 1}, Dims{3, 2, 2}) == 7);
+} END_TEST
+
+TEST_CPU("vcec_to_ecc prefix-sums and rejects an empty VCEC") {
+  GlobalVcec<float> v{{1, 2, 3}, {3, -1, -1}};
+  const auto c = vcec_to_ecc(v);
+  CHECK((c.chi == std::vector<std::int64_t>{3, 2, 1}));
+  CHECK_THROWS_WITH(vcec_to_ecc(GlobalVcec<float>{}), "empty VCEC");
+} END_TEST
+
+// ------------------------------------------------------------------ GPU
+TEST_GPU("staircase with two chunks gives {1:1, 2:0, 3:0, 4:0}") {  // test_streaming.cpp:84-89
+  const auto img = image_2d<float>({{1, 2}, {3, 4}});
+  const auto v = run_engine(img, 2);
+  CHECK((v.values == std::vector<float>{1, 2, 3, 4}));
+  CHECK((v.changes == std::vector<std::int64_t>{1, 0, 0, 0}));
+} END_TEST
+
+TEST_GPU("u8 merge keeps values that occur with zero net change") {  // :115-120
+  const auto img = image_2d<std::uint8_t>({{0, 0, 0}, {0, 9, 0}, {0, 0, 0}});
+  const auto v = run_engine(img, 1);
+  CHECK((v.values == std::vector<std::uint8_t>{0, 9}));
+  CHECK((v.changes == std::vector<std::int64_t>{0, 1}));
+} END_TEST
+
+TEST_GPU("ring curve (acceptance.cpp:182-198)") {
+  const auto img = image_2d<float>({{0, 0, 0}, {0, 9, 0}, {0, 0, 0}});
+  const auto c = vcec_to_ecc(run_engine(img));
+  CHECK((c.thresholds == std::vector<float>{0, 9}));
+  CHECK((c.chi == std::vector<std::int64_t>{0, 1}));
+} END_TEST
+
+TEST_GPU("random images: every type, every chunking == oracle") {
+  std::mt19937 rng(1);
+  for (int t = 0; t < 240; ++t) {
+    const Dims d = (t % 2) ? Dims{1 + rng() % 7, 1 + rng() % 7, 1 + rng() % 7}
+                           : Dims{1 + rng() % 9, 1 + rng() % 9, 1};
+    const auto n = d.voxel_count();
+    const int kind = t % 3;
+    for (std::uint64_t c : {std::uint64_t{1}, std::uint64_t{2}, std::uint64_t{3}, d.w0}) {
+      if (kind == 0) {
+        Image<std::uint8_t> img{d, {}};
+        for (std::uint64_t i = 0; i < n; ++i) img.values.push_back(rng() % 6);
+        CHECK(same(run_engine(img, c), oracle_vcec(img)));
+      } else if (kind == 1) {
+        Image<float> img{d, {}};
+        for (std::uint64_t i = 0; i < n; ++i) img.values.push_back(0.25f * (rng() % 5) - 0.5f);
+        CHECK(same(run_engine(img, c), oracle_vcec(img)));
+      } else {
+        Image<std::uint16_t> img{d, {}};
+        for (std::uint64_t i = 0; i < n; ++i) img.values.push_back(rng() % 5 * 9000);
+        CHECK(same(run_engine(img, c), oracle_vcec(img)));
+      }
+    }
+  }
+} END_TEST
+
+TEST_GPU("u8 and f32 paths agree on the same values (test_streaming.cpp:138-153)") {
+  std::mt19937 rng(7);
+  Image<std::uint8_t> u{{9, 13, 17}, {}};
+  Image<float> f{{9, 13, 17}, {}};
+  for (std::uint64_t i = 0; i < u.dims.voxel_count(); ++i) {
+    u.values.push_back(rng() % 256);
+    f.values.push_back(u.values.back());
+  }
+  const auto a = run_engine(u, 3);
+  const auto b = run_engine(f, 2);
+  CHECK(a.changes == b.changes);
+  CHECK(a.values.size() == b.values.size());
+  for (std::size_t i = 0; i < a.values.size(); ++i) CHECK(float(a.values[i]) == b.values[i]);
+} END_TEST
+
+TEST_GPU("a failing source names the chunk and the cause (test_streaming.cpp:164-198)") {
+  struct Flaky final : ChunkSource<float> {
+    Image<float> img;
+    Dims dims() const override { return img.dims; }
+    void read_rows(std::uint64_t r0, std::uint64_t r1, float* dst) override {
+      if (r1 > 5) throw std::runtime_error("simulated device failure");
+      std::memcpy(dst, img.values.data() + r0 * 9, (r1 - r0) * 9 * sizeof(float));
+    }
+  } src;
+  src.img.dims = {8, 3, 3};
+  src.img.values.assign(72, 1.0f);
+  const auto plan = plan_chunks<float>(src.img.dims, ChunkTarget::count(4));
+  CHECK_THROWS_WITH(process_image<float>(src, plan), "simulated device failure");
+  CHECK_THROWS_WITH(process_image<float>(src, plan), "chunk");
+} END_TEST
+
+TEST_GPU("invalid plans are rejected (streaming.hpp:186-195)") {
+  Image<float> img{{4, 1, 1}, {1, 2, 3, 4}};
+  CHECK_THROWS_WITH(process_image(img, ChunkPlan{}), "empty chunk plan");
+  CHECK_THROWS_WITH(process_image(img, ChunkPlan{{{0, 2}, {3, 4}}}), "contiguously");
+  CHECK_THROWS_WITH(process_image(img, ChunkPlan{{{0, 2}, {2, 3}}}), "w0 = 4");
+} END_TEST
+
+TEST_GPU("C1 synthetic 256x256 u8 (SURVEY.md Appendix B)") {
+  Image<std::uint8_t> img{{256, 256, 1}, std::vector<std::uint8_t>(65536)};
+  ecc_oracle_fill_u8(img.values.data(), 65536, 1, 0);
+  const auto c = device::curve(img.values.data(), img.dims);
+  CHECK(c.size() == 256);
+  CHECK(c.thresholds[0] == 0 && c.chi[0] == 238);
+  CHECK(c.chi.back() == 1);
+  CHECK(*std::min_element(c.chi.begin(), c.chi.end()) == -8214);
+  CHECK(*std::max_element(c.chi.begin(), c.chi.end()) == 4833);
+  CHECK(c == vcec_to_ecc(run_engine(img, 8)));
+} END_TEST
+
+TEST_GPU("3D u8 volumes through the fused fast path == oracle") {
+  std::mt19937 rng(3);
+  for (Dims d : {Dims{40, 35, 48}, Dims{7, 61, 64}, Dims{64, 64, 64}, Dims{2, 1, 16}}) {
+    Image<std::uint8_t> img{d, {}};
+    for (std::uint64_t i = 0; i < d.voxel_count(); ++i) img.values.push_back(rng() % 256);
+    const auto v = device::vcec(img.values.data(), d);
+    CHECK(same(v, oracle_vcec(img)));
+  }
+} END_TEST
+
+TEST_GPU("quantised f32 with the affine bin map (config 4 shape)") {
+  std::mt19937 rng(5);
+  Image<float> img{{20, 21, 22}, {}};
+  for (std::uint64_t i = 0; i < img.dims.voxel_count(); ++i)
+    img.values.push_back(float(rng() % 65536) * (1.0f / 65536.0f));
+  const BinMap bm = BinMap::affine(65536, 0.0f, 1.0f / 65536.0f);
+  CHECK(same(device::vcec(img.values.data(), img.dims, &bm), oracle_vcec(img)));
+  EngineOptions opt;
+  opt.bins = bm;
+  CHECK(same(process_image(img, plan_chunks<float>(img.dims, ChunkTarget::count(3)), opt),
+             oracle_vcec(img)));
+  img.values[5] = 0.3f;  // off the grid
+  CHECK_THROWS_WITH(device::vcec(img.values.data(), img.dims, &bm), "affine bin grid");
+} END_TEST
+
+TEST_GPU("batched 2D rows == per-image process_image") {
+  std::mt19937 rng(9);
+  const std::uint64_t count = 5, h = 33, w = 47;
+  std::vector<std::uint16_t> imgs(count * h * w);
+  for (auto& x : imgs) x = rng() % 700;
+  std::vector<std::int32_t> chi;
+  std::vector<std::uint32_t> pres;
+  device::batch2d(imgs.data(), count, h, w, chi, pres);
+  for (std::uint64_t b = 0; b < count; ++b) {
+    Image<std::uint16_t> one{{h, w, 1}, {imgs.begin() + b * h * w, imgs.begin() + (b + 1) * h * w}};
+    const auto want = vcec_to_ecc(run_engine(one, 2));
+    const auto got = device::batch_row_curve<std::uint16_t>(chi.data() + b * 65536,
+                                                            pres.data() + b * 2048, 65536);
+    CHECK(got.thresholds == want.thresholds);
+    CHECK(got.chi == want.chi);
+  }
+} END_TEST
+
+TEST_GPU("engine report has one timing per chunk") {
+  Image<std::uint8_t> img{{64, 32, 32}, std::vector<std::uint8_t>(64 * 32 * 32)};
+  ecc_oracle_fill_u8(img.values.data(), img.values.size(), 1, 0);
+  EngineReport rep;
+  const auto v = process_image(img, plan_chunks<std::uint8_t>(img.dims, ChunkTarget::count(4)),
+                               {}, &rep);
+  CHECK(v.total() == 1);
+  CHECK(rep.chunks.size() == 4);
+  for (const auto& t : rep.chunks) CHECK(t.kernel_end >= t.kernel_begin);
+} END_TEST
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "cpu";
+  int ran = 0;
+  for (auto& c : registry()) {
+    if (c.gpu != (mode == "gpu")) continue;
+    const int before = g_fail;
+    try {
+      c.fn();
+    } catch (const std::exception& e) {
+      ++g_fail;
+      std::printf("  exception: %s\n", e.what());
+    }
+    std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", c.name);
+    ++ran;
+  }
+  std::printf("%d cases, %d checks, %d failures\n", ran, g_checks, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

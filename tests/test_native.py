@@ -1,0 +1,48 @@
+"""The C++ side of the drop-in (include/ecc/*.hpp over the C ABI) and the
+bit-sliced helpers, exercised through the compiled C++ test programs in
+tests/cpp (built by __graft_entry__.build() / `make -C tests/cpp`)."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "bin")
+
+
+def _bin(name):
+    path = os.path.join(BIN, name)
+    if not os.path.exists(path):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    return path
+
+
+def _run(args, timeout=600):
+    p = subprocess.run(args, capture_output=True, text=True, timeout=timeout)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
+    return p.stdout
+
+
+def test_bit_sliced_sum_and_code_transpose():
+    out = _run([_bin("test_bits")])
+    assert "sum_code ok" in out and "transpose_codes ok" in out
+
+
+def test_cpp_api_host_cases():
+    out = _run([_bin("test_api"), "cpu"])
+    assert "0 failures" in out
+
+
+def test_cpp_headers_compile_standalone(tmp_path):
+    # every drop-in header is self-contained (includes what it uses)
+    for h in sorted(os.listdir(os.path.join(ROOT, "include", "ecc"))):
+        src = tmp_path / f"t_{h}.cpp"
+        src.write_text(f'#include "ecc/{h}"\nint main() {{ return 0; }}\n')
+        subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                        str(src)], check=True)
+
+
+@pytest.mark.gpu
+def test_cpp_api_gpu_cases():
+    out = _run([_bin("test_api"), "gpu"])
+    assert "0 failures" in out, out
