@@ -538,6 +538,8 @@ class Context:
         dt = {torch.uint8: ECC_U8, torch.uint16: ECC_U16, torch.float32: ECC_F32}[tensor.dtype]
         _check(lib().ecc_fill_synthetic(self._p, tensor.data_ptr(), dt, tensor.numel(), seed, base,
                                         stream or None))
+        if not stream:  # on the context's own stream: make it visible to torch's streams
+            torch.cuda.ExternalStream(self.stream, device=tensor.device).synchronize()
 
 
 _default_ctx = {}
