@@ -179,9 +179,10 @@ def main():
     dev = torch.device("cuda", local)
 
     # ---------------- data: this rank's slab + halo planes
+    from paper_2203_09087_b200.shard import shard_bounds, sharded_histogram
     W0 = SIDE * n
-    own0, own1 = SIDE * rank, SIDE * (rank + 1)
-    p0, p1 = max(own0 - 1, 0), min(own1 + 1, W0)
+    sh = shard_bounds(W0, n, rank)  # weak scaling: 512 planes per rank
+    own0, own1, p0, p1 = sh.own0, sh.own1, sh.plane0, sh.plane1
     dims = eb.Dims(W0, SIDE, SIDE)
     plane = SIDE * SIDE
     slab = torch.empty(((p1 - p0), SIDE, SIDE), dtype=torch.uint8, device=dev)
@@ -205,12 +206,16 @@ def main():
                     ev_k1.record(stream)
                 return
             hist.zero_()
-            if ev_k0 is not None:
-                ev_k0.record(stream)
-            ctx.accumulate_slab(slab, dims, p0, own0, own1, hist, stream=ctx.stream)
-            if ev_k1 is not None:
-                ev_k1.record(stream)
-            dist.all_reduce(hist)
+
+            def accumulate(shard, h):
+                if ev_k0 is not None:
+                    ev_k0.record(stream)
+                ctx.accumulate_slab(slab, dims, shard.plane0, shard.own0, shard.own1, h,
+                                    stream=ctx.stream)
+                if ev_k1 is not None:
+                    ev_k1.record(stream)
+
+            sharded_histogram(sh, accumulate, hist, dist.all_reduce)  # ONE all-reduce
             ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
 
     # correctness of what we time: final chi of a complete volume is 1

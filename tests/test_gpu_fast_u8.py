@@ -83,3 +83,34 @@ def test_config2_size_properties(ctx, golden):
     assert int(cur.chi[-1]) == 1 and cur.size() == 256
     assert int(cur.chi[0]) == 499566
     assert oracle.curve_digest(cur.thresholds, cur.chi) == golden["configs"]["C2"]["digest"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharded_driver_on_one_gpu(ctx, world):
+    """bench.py's N-rank step with the ranks run one after another on one GPU
+    (the all-reduce becomes a running sum): every rank count gives the same
+    curve, equal to the oracle's."""
+    import torch
+    from paper_2203_09087_b200.shard import shard_bounds, sharded_histogram
+    rng = np.random.default_rng(world)
+    img = rng.integers(0, 256, (37, 64, 96)).astype(np.uint8)
+    dims = eb.Dims.of(img.shape)
+    total = torch.zeros(512, dtype=torch.int64, device="cuda")
+    for r in range(world):
+        sh = shard_bounds(img.shape[0], world, r)
+        slab = torch.from_numpy(np.ascontiguousarray(img[sh.plane0:sh.plane1])).cuda()
+        h = torch.zeros(512, dtype=torch.int64, device="cuda")
+        sharded_histogram(sh, lambda s, hh: ctx.accumulate_slab(slab, dims, s.plane0, s.own0,
+                                                                 s.own1, hh), h,
+                          lambda hh: total.add_(hh))
+    bins = torch.empty(256, dtype=torch.int32, device="cuda")
+    chg = torch.empty(256, dtype=torch.int64, device="cuda")
+    chi = torch.empty(256, dtype=torch.int64, device="cuda")
+    cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+    ctx.finalize(total, 256, bins, chg, chi, cnt)
+    torch.cuda.synchronize()
+    m = int(cnt.item())
+    v, c = oracle.vcec(img)
+    assert np.array_equal(bins[:m].cpu().numpy(), v.astype(np.int32))
+    assert np.array_equal(chg[:m].cpu().numpy(), c)
+    assert np.array_equal(chi[:m].cpu().numpy(), np.cumsum(c))
