@@ -181,6 +181,18 @@ ECC_API int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* u
                        ecc_chunk_timing* timings, void* values_out,
                        int64_t* changes_out, uint64_t cap, uint64_t* n_out);
 
+/* process_image over a plan for an image that is already in HOST memory
+ * (streaming.hpp:181-338 with a MemorySource, chunk.hpp:139-152): each
+ * chunk's rows [own0 - 1, own1 + 1) are copied by DMA straight from `host`
+ * (page-locked memory gives full-speed asynchronous copies; pageable memory
+ * works but each copy then blocks) on the copy stream into one of three
+ * device slab buffers while the previous chunks' kernels run.  No
+ * read_rows callback and no staging copy.  Not valid for ECC_BIN_SORTED. */
+ECC_API int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims dims,
+                     const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
+                     ecc_chunk_timing* timings, void* values_out, int64_t* changes_out,
+                     uint64_t cap, uint64_t* n_out);
+
 /* ------------------------------------------------------------ batched 2D
  * New entry point (the reference has none): `count` images of
  * h x w (axis 0 = h), stored back to back.  For each image b, writes the

@@ -98,6 +98,9 @@ def lib() -> C.CDLL:
             L.ecc_accumulate_slab.argtypes = slab + [C.POINTER(_BinMap), _vp, _vp]
             L.ecc_compute_changes.argtypes = slab + [_vp, _vp]
             L.ecc_finalize.argtypes = [_vp, _vp, _u64, _vp, _vp, _vp, _vp, _vp]
+            L.ecc_process_host.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_u64), C.c_size_t,
+                                           C.POINTER(_BinMap), C.POINTER(_Timing), _vp, _vp, _u64,
+                                           C.POINTER(_u64)]
             L.ecc_curve_device.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp,
                                            _vp, _vp, _vp]
             vol = [_vp, _vp, C.c_int, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp, _u64, C.POINTER(_u64)]
@@ -110,7 +113,7 @@ def lib() -> C.CDLL:
             L.ecc_fill_synthetic.argtypes = [_vp, _vp, C.c_int, _u64, _u64, _u64, _vp]
             for n in ("ecc_ctx_create", "ecc_bin_count", "ecc_accumulate_slab", "ecc_compute_changes",
                       "ecc_finalize", "ecc_vcec", "ecc_curve", "ecc_process_stream", "ecc_batch2d",
-                      "ecc_fill_synthetic", "ecc_curve_device"):
+                      "ecc_fill_synthetic", "ecc_curve_device", "ecc_process_host"):
                 getattr(L, n).restype = C.c_int
             _lib = L
         return _lib
@@ -409,6 +412,42 @@ class Context:
         return EccCurve(t, chi)
 
     # -------------------------------------------------------------- streaming
+    def process_host(self, image, plan: ChunkPlan, report: EngineReport = None,
+                     binmap=None) -> GlobalVcec:
+        """process_image over a plan for a host array (ecc_process_host):
+        each chunk + halo rows is DMA-copied straight from `image` (page-locked
+        memory -- e.g. a pinned torch tensor's .numpy() -- streams at full
+        PCIe speed) while the previous chunks' kernels run."""
+        if not isinstance(image, np.ndarray):
+            image = image.numpy()
+        image = np.ascontiguousarray(image)
+        dt = _DT[image.dtype]
+        np_t = _NP[dt]
+        dims = Dims.of(image.shape)
+        ranges = plan.ranges
+        bounds = (_u64 * (len(ranges) + 1))()
+        if ranges:
+            bounds[0] = ranges[0].begin
+            for k, r in enumerate(ranges):
+                bounds[k + 1] = r.end
+                if k > 0 and r.begin != ranges[k - 1].end:
+                    raise EccError(ECC_EINVAL, "chunk plan does not cover the image contiguously")
+        bm = _binmap(dt, binmap)
+        cap = 256 if dt == ECC_U8 else (65536 if dt == ECC_U16 else max(1, bm.nbins))
+        vals = np.empty(cap, np_t)
+        ch = np.empty(cap, np.int64)
+        tim = (_Timing * max(1, len(ranges)))()
+        n = _u64()
+        _check(lib().ecc_process_host(self._p, image.ctypes.data, dt, _Dims(dims.w0, dims.w1, dims.w2),
+                                      bounds, len(ranges), C.byref(bm), tim, vals.ctypes.data,
+                                      ch.ctypes.data, cap, C.byref(n)))
+        if report is not None:
+            report.chunks = [ChunkTiming(ChunkRange(t.begin, t.end), t.ingest_begin, t.ingest_end,
+                                         t.index_begin, t.index_end, t.kernel_begin, t.kernel_end,
+                                         t.merge_begin, t.merge_end) for t in tim[:len(ranges)]]
+        m = n.value
+        return GlobalVcec(vals[:m].copy(), ch[:m].copy())
+
     def process_source(self, source: ChunkSource, plan: ChunkPlan, options: EngineOptions = None,
                        report: EngineReport = None, binmap=None) -> GlobalVcec:
         """process_image(ChunkSource&, plan) (streaming.hpp:181-329)."""

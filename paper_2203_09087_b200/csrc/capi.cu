@@ -123,7 +123,7 @@ struct ecc_ctx {
   uint64_t launches = 0;
   DevBuf input, hist, bins, changes, chi, count, flags;
   DevBuf keys, keys2, ch8, ch8b, sums, tmp;
-  DevBuf slab[2];
+  DevBuf slab[3];
   PinBuf staging[2];
   PinBuf host_small;
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
@@ -493,7 +493,8 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   cudaStreamSynchronize(ctx->copy);
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
-                    &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->fused})
+                    &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
+                    &ctx->fused})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -779,6 +780,107 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   *n_out = m;
   if (m > cap) return fail(ECC_EINVAL, "output capacity below the number of values");
   write_values(dtype, sorted, am, r, values_out);
+  std::memcpy(changes_out, r.changes.data(), m * 8);
+  return ECC_OK;
+}
+
+int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims dims,
+                     const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
+                     ecc_chunk_timing* timings, void* values_out, int64_t* changes_out,
+                     uint64_t cap, uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_dims(dims));
+  if (!host || !values_out || !changes_out || !n_out) return fail(ECC_EINVAL, "null pointer");
+  if (nchunks == 0 || !bounds) return fail(ECC_EINVAL, "empty chunk plan");
+  if (bounds[0] != 0) return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  for (size_t k = 0; k < nchunks; ++k)
+    if (bounds[k + 1] <= bounds[k])
+      return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  if (bounds[nchunks] != dims.w0)
+    return fail(ECC_EINVAL, "chunk plan covers [0, " + std::to_string(bounds[nchunks]) +
+                                ") but the source has w0 = " + std::to_string(dims.w0));
+  uint64_t nbins = 0;
+  bool affine = false, sorted = false;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  if (sorted)
+    return fail(ECC_EINVAL, "the sorted bin map streams through ecc_process_stream");
+  // pinned (page-locked or registered) memory is copied by DMA straight from
+  // the caller's buffer; pageable memory makes each copy synchronous
+  const auto t0 = std::chrono::steady_clock::now();
+  auto since = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const uint64_t row_bytes = dims.w1 * dims.w2 * esize(dtype);
+  uint64_t max_rows = 0;
+  for (size_t k = 0; k < nchunks; ++k)
+    max_rows = std::max<uint64_t>(max_rows, bounds[k + 1] - bounds[k] + 2);
+  max_rows = std::min<uint64_t>(max_rows, dims.w0);
+  constexpr int NB = 3;  // device slab buffers in flight
+  for (int b = 0; b < NB; ++b) CKI(ctx->slab[b].ensure(max_rows * row_bytes));
+  CKI(ctx->flags.ensure(4));
+  CKI(ctx->hist.ensure(2 * nbins * 8));
+  cudaStream_t st = ctx->stream, cp = ctx->copy;
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  std::vector<cudaEvent_t> ev(4 * nchunks + 1);
+  for (auto& e : ev) CKR(cudaEventCreate(&e));
+  auto evh0 = [&](size_t k) { return ev[4 * k + 0]; };  // H2D begin
+  auto evh1 = [&](size_t k) { return ev[4 * k + 1]; };  // H2D end
+  auto evk0 = [&](size_t k) { return ev[4 * k + 2]; };  // kernel begin
+  auto evk1 = [&](size_t k) { return ev[4 * k + 3]; };  // kernel end
+  cudaEvent_t start = ev[4 * nchunks];
+  CKR(cudaEventRecord(start, cp));
+  const double t_start = since();
+  int rc = ECC_OK;
+  for (size_t k = 0; k < nchunks && rc == ECC_OK; ++k) {
+    const int b = (int)(k % NB);
+    const uint64_t own0 = bounds[k], own1 = bounds[k + 1];
+    const uint64_t r0 = own0 == 0 ? 0 : own0 - 1;
+    const uint64_t r1 = std::min<uint64_t>(own1 + 1, dims.w0);
+    if (k >= (size_t)NB) CKR(cudaStreamWaitEvent(cp, evk1(k - NB), 0));  // buffer reuse
+    CKR(cudaEventRecord(evh0(k), cp));
+    CKR(cudaMemcpyAsync(ctx->slab[b].p, static_cast<const uint8_t*>(host) + r0 * row_bytes,
+                        (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, cp));
+    CKR(cudaEventRecord(evh1(k), cp));
+    CKR(cudaStreamWaitEvent(st, evh1(k), 0));
+    CKR(cudaEventRecord(evk0(k), st));
+    const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
+    rc = accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st);
+    CKR(cudaEventRecord(evk1(k), st));
+  }
+  BinResult r;
+  if (rc == ECC_OK) {
+    rc = finalize_to_host(ctx, (uint32_t)nbins, st, &r);
+    if (rc == ECC_OK) rc = read_flags(ctx, st);
+  }
+  CKR(cudaStreamSynchronize(cp));
+  CKR(cudaStreamSynchronize(st));
+  if (rc == ECC_OK && timings) {
+    for (size_t k = 0; k < nchunks; ++k) {
+      float a = 0, b = 0, c = 0, d = 0;
+      CKR(cudaEventElapsedTime(&a, start, evh0(k)));
+      CKR(cudaEventElapsedTime(&b, start, evh1(k)));
+      CKR(cudaEventElapsedTime(&c, start, evk0(k)));
+      CKR(cudaEventElapsedTime(&d, start, evk1(k)));
+      ecc_chunk_timing& t = timings[k];
+      t.begin = bounds[k];
+      t.end = bounds[k + 1];
+      t.ingest_begin = t_start + a * 1e-3;
+      t.ingest_end = t_start + b * 1e-3;
+      t.index_begin = t.index_end = t.ingest_end;
+      t.kernel_begin = t_start + c * 1e-3;
+      t.kernel_end = t_start + d * 1e-3;
+      t.merge_begin = t.merge_end = t.kernel_end;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (rc != ECC_OK) return rc;
+  const size_t m = r.changes.size();
+  *n_out = m;
+  if (m > cap) return fail(ECC_EINVAL, "output capacity below the number of values");
+  write_values(dtype, false, am, r, values_out);
   std::memcpy(changes_out, r.changes.data(), m * 8);
   return ECC_OK;
 }

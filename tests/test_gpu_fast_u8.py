@@ -102,7 +102,7 @@ def test_sharded_driver_on_one_gpu(ctx, world):
         h = torch.zeros(512, dtype=torch.int64, device="cuda")
         sharded_histogram(sh, lambda s, hh: ctx.accumulate_slab(slab, dims, s.plane0, s.own0,
                                                                  s.own1, hh), h,
-                          lambda hh: total.add_(hh))
+                          lambda hh: (torch.cuda.synchronize(), total.add_(hh)))
     bins = torch.empty(256, dtype=torch.int32, device="cuda")
     chg = torch.empty(256, dtype=torch.int64, device="cuda")
     chi = torch.empty(256, dtype=torch.int64, device="cuda")

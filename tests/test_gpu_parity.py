@@ -244,3 +244,52 @@ def test_stream_reports_timings_and_overlap(ctx):
                max(rep.chunks[k].kernel_begin, rep.chunks[k + 1].ingest_begin) or
                rep.chunks[k + 1].ingest_begin < rep.chunks[k].kernel_end
                for k in range(3))
+
+
+def test_process_host_direct_dma(ctx):
+    """ecc_process_host: chunks + halos DMA'd straight from a (pinned) host
+    buffer, three device slabs in flight; every type it supports, several
+    plans, against the oracle."""
+    import torch
+    rng = np.random.default_rng(77)
+    cases = [rng.integers(0, 256, (37, 40, 48)).astype(np.uint8),        # fast u8 path
+             rng.integers(0, 256, (23, 17, 19)).astype(np.uint8),        # generic u8
+             rng.integers(0, 3000, (15, 21, 9)).astype(np.uint16),
+             rng.integers(0, 256, (30, 40, 1)).astype(np.uint8)]         # 2D
+    for img in cases:
+        want = oracle.vcec(img)
+        pinned = torch.from_numpy(img).pin_memory().numpy()
+        for c in (1, 2, 5, img.shape[0]):
+            plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(c))
+            rep = eb.EngineReport()
+            got = ctx.process_host(pinned, plan, report=rep)
+            assert _same(got.values, got.changes, *want), (img.shape, c)
+            assert len(rep.chunks) == len(plan.ranges)
+    q = (rng.integers(0, 65536, (12, 10, 14)) * 2.0 ** -16).astype(np.float32)
+    got = ctx.process_host(q, eb.plan_chunks(eb.Dims.of(q.shape), eb.ChunkTarget.count(3)),
+                           binmap=eb.quantised_binmap(65536))
+    assert _same(got.values, got.changes, *oracle.vcec(q))
+
+
+@pytest.mark.slow
+def test_config5_first_64_planes_streamed(ctx, golden):
+    import torch
+    side = 4096
+    host = torch.empty((64, side, side), dtype=torch.uint8, pin_memory=True)
+    dev = torch.empty((64, side, side), dtype=torch.uint8, device="cuda")
+    ctx.fill_synthetic(dev, seed=1)
+    host.copy_(dev)
+    del dev
+    v = ctx.process_host(host.numpy(), eb.plan_chunks(eb.Dims(64, side, side), eb.ChunkTarget.count(8)))
+    cur = eb.vcec_to_ecc(v)
+    assert oracle.curve_digest(cur.thresholds, cur.chi) == golden["configs"]["C5_64"]["digest"]
+
+
+@pytest.mark.slow
+def test_config4_golden_device_resident(ctx, golden):
+    import torch
+    vol = torch.empty((1024, 1024, 1024), dtype=torch.float32, device="cuda")
+    ctx.fill_synthetic(vol, seed=1)
+    c = ctx.curve(vol, binmap=eb.quantised_binmap(65536))
+    assert oracle.curve_digest(c.thresholds, c.chi) == golden["configs"]["C4"]["digest"]
+    assert c.size() == 65536 and int(c.chi[-1]) == 1
