@@ -61,12 +61,23 @@ __host__ __device__ __forceinline__ uint32_t bsel(uint32_t a, uint32_t m, uint32
 #endif
 }
 
+// x >> k computed on the FMA pipe (IMAD.HI: the high word of x * 2^(32-k))
+// instead of the integer ALU pipe, which is the stencil kernel's bottleneck.
+__host__ __device__ __forceinline__ uint32_t shr_fma(uint32_t x, int k) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(x, 1u << (32 - k));
+#else
+  return x >> k;
+#endif
+}
+
 // Merge-style delta swap between w[i] and w[i+s] on bit distance `sh` with
-// mask m (bits that stay in w[i]): one shift + one lop3 per output word.
+// mask m (bits that stay in w[i]): one shift + one lop3 per output word
+// (the left shift becomes IMAD.SHL, the right one IMAD.HI: both FMA pipe).
 __host__ __device__ __forceinline__ void dswap(uint32_t& lo, uint32_t& hi, int sh, uint32_t m) {
   const uint32_t a = lo, b = hi;
   lo = bsel(a, m, b << sh);
-  hi = bsel(a >> sh, m, b);
+  hi = bsel(shr_fma(a, sh), m, b);
 }
 
 // 8x8 bit-matrix transpose applied to the four bytes of 8 words in

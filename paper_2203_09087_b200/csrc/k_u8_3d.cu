@@ -256,7 +256,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
   {
     uint32_t Cz[8], Cy[8], mzy[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) Cz[i] = C[i] >> 1;
+    for (int i = 0; i < 8; ++i) Cz[i] = bits::shr_fma(C[i], 1);
     uint32_t gz = bits::gt<8>(C, Cz);
     if (rg.zlo) gz |= 1u;  // z = -1 never wins as the lower side
     bits::sel<8>(N.mz, gz, C, Cz);
