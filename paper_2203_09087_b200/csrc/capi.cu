@@ -21,7 +21,8 @@ using namespace eccb;
 
 namespace eccb {
 cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, int w,
-                           int32_t* chi, uint32_t* presence, cudaStream_t st);
+                           int32_t* chi, uint32_t* presence, int32_t* spill_scratch,
+                           cudaStream_t st);
 cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
                                    const AffineMap& am, int64_t* ghist,
                                    uint32_t nbins, uint32_t* flags, int sms,
@@ -127,6 +128,7 @@ struct ecc_ctx {
   PinBuf staging[2];
   PinBuf host_small;
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
+  DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
 
 namespace {
@@ -455,6 +457,17 @@ int stage_input(ecc_ctx* ctx, const void* data, int where, uint64_t bytes,
   return ECC_OK;
 }
 
+// Spill rows of the u16 batched kernel: one int32[65536] row per SM id
+// (%smid < 256 on every part this targets), zeroed once and kept zero by
+// the kernel itself.
+int batch_scratch(ecc_ctx* ctx, ecc_dtype dtype, cudaStream_t st) {
+  if (dtype != ECC_U16 || ctx->bscratch.p) return ECC_OK;
+  const size_t bytes = 256ull * 65536 * 4;
+  CKI(ctx->bscratch.ensure(bytes));
+  CKR(cudaMemsetAsync(ctx->bscratch.p, 0, bytes, st));
+  return ECC_OK;
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -494,7 +507,7 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
-                    &ctx->fused})
+                    &ctx->fused, &ctx->bscratch})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -897,7 +910,9 @@ int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, uint
   cudaStream_t st = pick(ctx, stream);
   const uint64_t nbins = dtype == ECC_U8 ? 256 : 65536;
   if (where == 1) {
-    CKR(launch_batch2d(data, (int)dtype, count, (int)h, (int)w, chi, presence, st));
+    CKI(batch_scratch(ctx, dtype, st));
+    CKR(launch_batch2d(data, (int)dtype, count, (int)h, (int)w, chi, presence,
+                       ctx->bscratch.as<int32_t>(), st));
     ctx->launches += 1;
     return ECC_OK;
   }
@@ -907,8 +922,9 @@ int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, uint
   CKI(ctx->chi.ensure(count * nbins * 4));
   CKI(ctx->bins.ensure(count * nbins / 8));
   CKR(cudaMemcpyAsync(ctx->input.p, data, in_bytes, cudaMemcpyHostToDevice, st));
+  CKI(batch_scratch(ctx, dtype, st));
   CKR(launch_batch2d(ctx->input.p, (int)dtype, count, (int)h, (int)w, ctx->chi.as<int32_t>(),
-                     ctx->bins.as<uint32_t>(), st));
+                     ctx->bins.as<uint32_t>(), ctx->bscratch.as<int32_t>(), st));
   ctx->launches += 1;
   CKR(cudaMemcpyAsync(chi, ctx->chi.p, count * nbins * 4, cudaMemcpyDeviceToHost, st));
   CKR(cudaMemcpyAsync(presence, ctx->bins.p, count * nbins / 8, cudaMemcpyDeviceToHost, st));

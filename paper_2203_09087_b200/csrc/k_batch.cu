@@ -1,13 +1,21 @@
 // k_batch.cu -- batched 2D ECC (the reference has no
 // in-memory batched entry point; BASELINE config 3 needs one).
 //
-// One CTA per image.  The histogram of per-pixel changes (change_2d,
-// kernel.hpp:81-94) is built in the output row itself and then prefix-summed
-// in place, so each image's curve is produced without leaving the CTA:
-//   * <= 8192 bins (u8): shared-memory bins, one flush per CTA;
-//   * 65536 bins (u16): packed 16-bit bin pairs in shared memory (128 KB)
-//     plus an 8 KB presence bitmap, with exact overflow spill to the global
-//     row (see PackedBins below).
+// One CTA per image (1024 threads).  Thread t owns column j = t % w of a
+// band of rows and slides a 3 x 3 key window down it (one new row of three
+// values per step, prefetched one step ahead), evaluating change_2d
+// (kernel.hpp:81-94) per pixel.  The per-image histogram lives in shared
+// memory:
+//   * <= 8192 bins (u8): int32 change sums + occupancy bits;
+//   * 65536 bins (u16): signed 16-bit halves packed two per word (128 KB)
+//     with exact spill: the thread whose atomic carries a half out of
+//     [-16384, 16383] subtracts what it saw and adds it to a per-SM global
+//     scratch row (one CTA per SM, so rows are private), marking the bin in
+//     a "spilled" bitmap so the epilogue reads back and re-zeroes exactly
+//     those scratch entries.
+// The epilogue prefix-sums the bins in place (block scan over per-thread
+// runs) and writes the dense chi row and the occupancy bitmap -- one pass,
+// no zero-fill of the output.
 #include <cub/cub.cuh>
 
 #include "ecc_common.cuh"
@@ -17,134 +25,160 @@ namespace eccb {
 
 namespace {
 
-template <class T>
-__device__ __forceinline__ uint32_t key_at(const T* img, int h, int w, int i,
-                                           int j) {
-  if (i < 0 || i >= h || j < 0 || j >= w) return KeyTraits<T>::kSentinel;
-  return KeyTraits<T>::key(__ldg(img + (size_t)i * w + j));
-}
+constexpr int NT = 1024;
 
-// Shared-memory bins for 65536 values in 128 KB: word q holds bins 2q (low
-// half) and 2q+1 (high half) as one integer V = S_lo + 65536 * S_hi, which
-// an atomicAdd of `change` or `change << 16` updates exactly.  The halves
-// decode unambiguously while each |S| < 32768.  Every change moves a half
-// by at most 3 (2D range [-3, 1]); the thread whose update
-// carries a half out of [-16384, 16383] subtracts exactly what it observed
-// and spills it to the global row, so halves never get near the limit.
 __device__ __forceinline__ int sext16(uint32_t v) { return (int)(int16_t)(v & 0xFFFF); }
 
-__device__ __forceinline__ void packed_add(uint32_t* words, uint32_t bin, int ch,
-                                           int32_t* grow) {
-  const uint32_t q = bin >> 1;
-  const bool hi = bin & 1;
-  const uint32_t add = hi ? ((uint32_t)ch << 16) : (uint32_t)ch;
-  const uint32_t old = atomicAdd(&words[q], add);
-  const uint32_t nw = old + add;
-  // decode the touched half before and after
-  const int lo_old = sext16(old), lo_new = sext16(nw);
-  int before, after;
-  if (hi) {
-    before = (int)((int32_t)(old - (uint32_t)lo_old) >> 16);
-    after = (int)((int32_t)(nw - (uint32_t)lo_new) >> 16);
-  } else {
-    before = lo_old;
-    after = lo_new;
-  }
-  const bool in_before = before >= -16384 && before <= 16383;
-  const bool in_after = after >= -16384 && after <= 16383;
-  if (in_before && !in_after) {
-    atomicAdd(&words[q], hi ? (uint32_t)(-after) << 16 : (uint32_t)(-after));
-    atomicAdd(&grow[bin], after);
-  }
+__device__ __forceinline__ int half_of(uint32_t word, bool hi) {
+  const int lo = sext16(word);
+  return hi ? (int)((int32_t)(word - (uint32_t)lo) >> 16) : lo;
+}
+
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// change_2d over axes 0 and 1 (kernel.hpp:81-94): w[a][b] = offset (a-1, b-1)
+__device__ __forceinline__ int change2k(const uint32_t (&w)[3][3]) {
+  const uint32_t c = w[1][1];
+  const int am = c < w[0][1], ap = c <= w[2][1];
+  const int bm = c < w[1][0], bp = c <= w[1][2];
+  const int v = (am & bm & (c < w[0][0])) + (am & bp & (c < w[0][2])) +
+                (ap & bm & (c <= w[2][0])) + (ap & bp & (c <= w[2][2]));
+  return 1 + v - (am + ap + bm + bp);
 }
 
 }  // namespace
 
 template <class T, bool PACKED>
-__global__ void __launch_bounds__(1024) k_batch2d(const T* __restrict__ data, int h,
-                                                  int w, uint32_t nbins,
-                                                  int32_t* __restrict__ chi,
-                                                  uint32_t* __restrict__ presence) {
+__global__ void __launch_bounds__(NT, 1)
+    k_batch2d(const T* __restrict__ data, int h, int w, uint32_t nbins, int32_t* __restrict__ chi,
+              uint32_t* __restrict__ presence, int32_t* __restrict__ spill_scratch) {
   extern __shared__ uint32_t sm[];
-  const size_t img_id = blockIdx.x;
-  const T* img = data + img_id * (size_t)h * w;
-  int32_t* row = chi + img_id * (size_t)nbins;
-  uint32_t* pres_row = presence + img_id * (size_t)(nbins / 32);
   const uint32_t nwords = PACKED ? nbins / 2 : nbins;
   uint32_t* bins = sm;
   uint32_t* pres = sm + nwords;
-  for (uint32_t q = threadIdx.x; q < nwords + nbins / 32; q += blockDim.x) sm[q] = 0;
-  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) row[b] = 0;
+  uint32_t* spilled = pres + nbins / 32;  // PACKED only
+  const uint32_t nsm = nwords + nbins / 32 + (PACKED ? nbins / 32 : 0);
+  for (uint32_t q = threadIdx.x; q < nsm; q += NT) sm[q] = 0;
   __syncthreads();
-  // pixels in row-major order, a 3x3 key window per pixel
-  const int n = h * w;
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    const int i = p / w, j = p - i * w;
-    uint32_t win[3][3];
+  const T* img = data + (size_t)blockIdx.x * h * w;
+  int32_t* row = chi + (size_t)blockIdx.x * nbins;
+  uint32_t* pres_row = presence + (size_t)blockIdx.x * (nbins / 32);
+  int32_t* scratch = PACKED ? spill_scratch + (size_t)smid() * nbins : nullptr;
+  constexpr uint32_t SENT = KeyTraits<T>::kSentinel;
+
+  // thread -> (column, band of rows)
+  const int bands = max(1, NT / w);
+  const int cols_per_pass = NT / bands;  // >= w when bands > 1
+  for (int j0 = 0; j0 < w; j0 += cols_per_pass) {
+    const int j = j0 + (int)threadIdx.x % cols_per_pass;
+    const int band = (int)threadIdx.x / cols_per_pass;
+    if (j >= w || band >= bands) continue;
+    const int rows = (h + bands - 1) / bands;
+    const int i0 = band * rows, i1 = min(h, i0 + rows);
+    if (i0 >= i1) continue;
+    const bool lv = j >= 1, rv = j + 1 < w;
+    // one running pointer per thread; rows outside the image read the
+    // sentinel (the loop bounds keep the pointer inside for i in [0, h))
+    const T* p = img + (ptrdiff_t)(i0 - 1) * w + j;
+    auto fetch = [&](int i, const T* q, uint32_t (&r)[3]) {
+      if (i < 0 || i >= h) {
+        r[0] = r[1] = r[2] = SENT;
+        return;
+      }
+      r[0] = lv ? (uint32_t)__ldg(q - 1) : SENT;
+      r[1] = (uint32_t)__ldg(q);
+      r[2] = rv ? (uint32_t)__ldg(q + 1) : SENT;
+    };
+    uint32_t win[3][3], nxt[3];
+    fetch(i0 - 1, p, win[0]);
+    fetch(i0, p + w, win[1]);
+    fetch(i0 + 1, p + 2 * w, nxt);
+    p += 3 * w;  // row i0 + 2
+    for (int i = i0; i < i1; ++i, p += w) {
+      win[2][0] = nxt[0];
+      win[2][1] = nxt[1];
+      win[2][2] = nxt[2];
+      fetch(i + 2, p, nxt);  // prefetch
+      const int ch = change2k(win);
+      const uint32_t v = win[1][1];
+      // occupancy: a plain load first; the atomic only the first time
+      if (!((pres[v >> 5] >> (v & 31)) & 1u)) atomicOr(&pres[v >> 5], 1u << (v & 31));
+      if (ch != 0) {
+        if constexpr (PACKED) {
+          const uint32_t q = v >> 1;
+          const bool hi = v & 1;
+          const uint32_t add = hi ? ((uint32_t)ch << 16) : (uint32_t)ch;
+          const uint32_t old = atomicAdd(&bins[q], add);
+          const int before = half_of(old, hi), after = half_of(old + add, hi);
+          const bool in_b = before >= -16384 && before <= 16383;
+          const bool in_a = after >= -16384 && after <= 16383;
+          if (in_b && !in_a) {
+            atomicAdd(&bins[q], hi ? (uint32_t)(-after) << 16 : (uint32_t)(-after));
+            atomicAdd(&scratch[v], after);
+            atomicOr(&spilled[v >> 5], 1u << (v & 31));
+          }
+        } else {
+          atomicAdd(&bins[v], (uint32_t)ch);
+        }
+      }
 #pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) win[a][b] = key_at<T>(img, h, w, i - 1 + a, j - 1 + b);
-    const int ch = change2(win);
-    const uint32_t v = win[1][1];
-    atomicOr(&pres[v >> 5], 1u << (v & 31));
-    if (ch != 0) {
-      if constexpr (PACKED)
-        packed_add(bins, v, ch, row);
-      else
-        atomicAdd(&bins[v], (uint32_t)ch);
+      for (int b = 0; b < 3; ++b) {
+        win[0][b] = win[1][b];
+        win[1][b] = win[2][b];
+      }
     }
   }
   __syncthreads();
-  // fold shared bins into the row (spills already there), then scan in place
-  const uint32_t per = (nbins + blockDim.x - 1) / blockDim.x;
+  // epilogue: thread t owns bins [t * per, (t + 1) * per)
+  const uint32_t per = (nbins + NT - 1) / NT;
   const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
-  int32_t local = 0;
-  for (uint32_t b = b0; b < b1; ++b) {
-    int s;
+  auto bin_sum = [&](uint32_t b) -> int {
     if constexpr (PACKED) {
-      const uint32_t word = bins[b >> 1];
-      const int lo = sext16(word);
-      s = (b & 1) ? (int)((int32_t)(word - (uint32_t)lo) >> 16) : lo;
+      int s = half_of(bins[b >> 1], b & 1);
+      if ((spilled[b >> 5] >> (b & 31)) & 1u) s += scratch[b];
+      return s;
     } else {
-      s = (int)bins[b];
+      return (int)bins[b];
     }
-    local += s + row[b];
-  }
-  using Scan = cub::BlockScan<int32_t, 1024>;
+  };
+  int32_t local = 0;
+  for (uint32_t b = b0; b < b1; ++b) local += bin_sum(b);
+  using Scan = cub::BlockScan<int32_t, NT>;
   __shared__ typename Scan::TempStorage tmp;
   int32_t ex;
   Scan(tmp).ExclusiveSum(local, ex);
   for (uint32_t b = b0; b < b1; ++b) {
-    int s;
-    if constexpr (PACKED) {
-      const uint32_t word = bins[b >> 1];
-      const int lo = sext16(word);
-      s = (b & 1) ? (int)((int32_t)(word - (uint32_t)lo) >> 16) : lo;
-    } else {
-      s = (int)bins[b];
-    }
-    ex += s + row[b];
+    ex += bin_sum(b);
     row[b] = ex;
   }
-  for (uint32_t q = threadIdx.x; q < nbins / 32; q += blockDim.x) pres_row[q] = pres[q];
+  if constexpr (PACKED) {
+    __syncthreads();  // all reads of the scratch row are done
+    for (uint32_t b = b0; b < b1; ++b)
+      if ((spilled[b >> 5] >> (b & 31)) & 1u) scratch[b] = 0;
+  }
+  for (uint32_t q = threadIdx.x; q < nbins / 32; q += NT) pres_row[q] = pres[q];
 }
 
 cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, int w,
-                           int32_t* chi, uint32_t* presence, cudaStream_t st) {
+                           int32_t* chi, uint32_t* presence, int32_t* spill_scratch,
+                           cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   if (dtype == 0) {
     const uint32_t nbins = 256;
     const size_t smem = (nbins + nbins / 32) * 4;
-    k_batch2d<uint8_t, false><<<(unsigned)count, 1024, smem, st>>>(
-        (const uint8_t*)data, h, w, nbins, chi, presence);
+    k_batch2d<uint8_t, false><<<(unsigned)count, NT, smem, st>>>(
+        (const uint8_t*)data, h, w, nbins, chi, presence, nullptr);
   } else if (dtype == 1) {
     const uint32_t nbins = 65536;
-    const size_t smem = (nbins / 2 + nbins / 32) * 4;
+    const size_t smem = (nbins / 2 + 2 * nbins / 32) * 4;
     cudaFuncSetAttribute(k_batch2d<uint16_t, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_batch2d<uint16_t, true><<<(unsigned)count, 1024, smem, st>>>(
-        (const uint16_t*)data, h, w, nbins, chi, presence);
+    k_batch2d<uint16_t, true><<<(unsigned)count, NT, smem, st>>>(
+        (const uint16_t*)data, h, w, nbins, chi, presence, spill_scratch);
   } else {
     return cudaErrorInvalidValue;
   }
