@@ -207,6 +207,53 @@ GlobalVcec<T> process_image(ChunkSource<T>& source, const ChunkPlan& plan,
   }
 }
 
+// A FileSource streams through the GPU file path (ecc_process_file): chunked
+// pread into pinned staging, f32 byte swap + NaN rejection on the device,
+// the reference's error wording.
+template <class T>
+GlobalVcec<T> process_image(FileSource<T>& source, const ChunkPlan& plan,
+                            const EngineOptions& opt = {}, EngineReport* report = nullptr) {
+  const Dims dims = source.dims();
+  if (plan.ranges.empty()) throw error("empty chunk plan");
+  std::vector<std::uint64_t> bounds{plan.ranges.front().begin};
+  for (const auto& r : plan.ranges) bounds.push_back(r.end);
+  Context& ctx = Context::on(opt.device);
+  ecc_binmap b;
+  const BinMap* bm = opt.bins ? &*opt.bins : nullptr;
+  const ecc_binmap* pb = detail::binmap_for<T>(bm, b);
+  std::uint64_t cap = 0;
+  if (b.kind == ECC_BIN_SORTED)
+    cap = std::min<std::uint64_t>(dims.voxel_count(), 1ull << 22);
+  else
+    detail::check(ecc_bin_count(detail::dtype_of<T>::value, pb, &cap));
+  std::vector<ecc_chunk_timing> tim(plan.ranges.size());
+  for (;;) {
+    GlobalVcec<T> out;
+    out.values.resize(cap);
+    out.changes.resize(cap);
+    std::uint64_t n = 0;
+    const int rc = ecc_process_file(ctx.get(), source.path().c_str(), detail::dtype_of<T>::value,
+                                    detail::cdims(dims), source.options().big_endian ? 1 : 0,
+                                    bounds.data(), plan.ranges.size(), pb, tim.data(),
+                                    out.values.data(), out.changes.data(), cap, &n);
+    if (rc != ECC_OK && n > cap) {
+      cap = n;
+      continue;
+    }
+    detail::check(rc);
+    out.values.resize(n);
+    out.changes.resize(n);
+    if (report) {
+      report->chunks.clear();
+      for (const auto& t : tim)
+        report->chunks.push_back({{t.begin, t.end}, t.ingest_begin, t.ingest_end, t.index_begin,
+                                  t.index_end, t.kernel_begin, t.kernel_end, t.merge_begin,
+                                  t.merge_end});
+    }
+    return out;
+  }
+}
+
 // Convenience wrapper for whole in-memory images (streaming.hpp:332-338).
 template <class T>
 GlobalVcec<T> process_image(const Image<T>& image, const ChunkPlan& plan,

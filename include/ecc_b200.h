@@ -193,6 +193,18 @@ ECC_API int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ec
                      ecc_chunk_timing* timings, void* values_out, int64_t* changes_out,
                      uint64_t cap, uint64_t* n_out);
 
+/* process_image over a FileSource (chunk.hpp:154-189, image.hpp:39-52): a
+ * raw row-major file of dtype elements with `dims` (size checked with the
+ * reference's message), read chunk by chunk (pread into pinned staging,
+ * overlapped with the previous chunk's device work).  For f32 the byte swap
+ * of big-endian files and the NaN check run on the device after the copy; a
+ * NaN fails the call with "ingestion of chunk k failed: NaN value at linear
+ * index i" (the first chunk, in plan order, whose rows hold one). */
+ECC_API int ecc_process_file(ecc_ctx* ctx, const char* path, ecc_dtype dtype, ecc_dims dims,
+                     int big_endian, const uint64_t* bounds, size_t nchunks,
+                     const ecc_binmap* bm, ecc_chunk_timing* timings, void* values_out,
+                     int64_t* changes_out, uint64_t cap, uint64_t* n_out);
+
 /* ------------------------------------------------------------ batched 2D
  * New entry point (the reference has none): `count` images of
  * h x w (axis 0 = h), stored back to back.  For each image b, writes the

@@ -101,6 +101,9 @@ def lib() -> C.CDLL:
             L.ecc_process_host.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_u64), C.c_size_t,
                                            C.POINTER(_BinMap), C.POINTER(_Timing), _vp, _vp, _u64,
                                            C.POINTER(_u64)]
+            L.ecc_process_file.argtypes = [_vp, C.c_char_p, C.c_int, _Dims, C.c_int, C.POINTER(_u64),
+                                           C.c_size_t, C.POINTER(_BinMap), C.POINTER(_Timing), _vp,
+                                           _vp, _u64, C.POINTER(_u64)]
             L.ecc_curve_device.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp,
                                            _vp, _vp, _vp]
             vol = [_vp, _vp, C.c_int, C.c_int, _Dims, C.POINTER(_BinMap), _vp, _vp, _u64, C.POINTER(_u64)]
@@ -113,7 +116,8 @@ def lib() -> C.CDLL:
             L.ecc_fill_synthetic.argtypes = [_vp, _vp, C.c_int, _u64, _u64, _u64, _vp]
             for n in ("ecc_ctx_create", "ecc_bin_count", "ecc_accumulate_slab", "ecc_compute_changes",
                       "ecc_finalize", "ecc_vcec", "ecc_curve", "ecc_process_stream", "ecc_batch2d",
-                      "ecc_fill_synthetic", "ecc_curve_device", "ecc_process_host"):
+                      "ecc_fill_synthetic", "ecc_curve_device", "ecc_process_host",
+                      "ecc_process_file"):
                 getattr(L, n).restype = C.c_int
             _lib = L
         return _lib
@@ -441,6 +445,38 @@ class Context:
         _check(lib().ecc_process_host(self._p, image.ctypes.data, dt, _Dims(dims.w0, dims.w1, dims.w2),
                                       bounds, len(ranges), C.byref(bm), tim, vals.ctypes.data,
                                       ch.ctypes.data, cap, C.byref(n)))
+        if report is not None:
+            report.chunks = [ChunkTiming(ChunkRange(t.begin, t.end), t.ingest_begin, t.ingest_end,
+                                         t.index_begin, t.index_end, t.kernel_begin, t.kernel_end,
+                                         t.merge_begin, t.merge_end) for t in tim[:len(ranges)]]
+        m = n.value
+        return GlobalVcec(vals[:m].copy(), ch[:m].copy())
+
+    def process_file(self, path: str, dims: Dims, dtype, plan: ChunkPlan = None,
+                     big_endian: bool = False, binmap=None,
+                     report: EngineReport = None) -> GlobalVcec:
+        """process_image over the reference's FileSource (chunk.hpp:154-189):
+        raw row-major file, chunked pread into pinned staging; f32 byte swap
+        and NaN rejection run on the GPU (ecc_process_file)."""
+        dt = _DT[np.dtype(dtype)]
+        np_t = _NP[dt]
+        plan = plan or _even_plan(dims.w0, 1)
+        ranges = plan.ranges
+        bounds = (_u64 * (len(ranges) + 1))()
+        if ranges:
+            bounds[0] = ranges[0].begin
+            for k, r in enumerate(ranges):
+                bounds[k + 1] = r.end
+        bm = _binmap(dt, binmap)
+        cap = 256 if dt == ECC_U8 else (65536 if dt == ECC_U16 else
+                                         (bm.nbins if bm.kind == ECC_BIN_AFFINE else dims.voxel_count()))
+        vals = np.empty(max(1, cap), np_t)
+        ch = np.empty(max(1, cap), np.int64)
+        tim = (_Timing * max(1, len(ranges)))()
+        n = _u64()
+        _check(lib().ecc_process_file(self._p, os.fsencode(path), dt, _Dims(dims.w0, dims.w1, dims.w2),
+                                      int(big_endian), bounds, len(ranges), C.byref(bm), tim,
+                                      vals.ctypes.data, ch.ctypes.data, cap, C.byref(n)))
         if report is not None:
             report.chunks = [ChunkTiming(ChunkRange(t.begin, t.end), t.ingest_begin, t.ingest_end,
                                          t.index_begin, t.index_end, t.kernel_begin, t.kernel_end,

@@ -11,6 +11,10 @@
 #include <string>
 #include <vector>
 
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cub/cub.cuh>
 #include <thrust/iterator/transform_iterator.h>
 
@@ -23,6 +27,8 @@ namespace eccb {
 cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, int w,
                            int32_t* chi, uint32_t* presence, int32_t* spill_scratch,
                            cudaStream_t st);
+cudaError_t launch_fixup(void* d, int dtype, uint64_t n, uint64_t base, bool big_endian,
+                         unsigned long long* nan_min, int sms, cudaStream_t st);
 cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
                                    const AffineMap& am, int64_t* ghist,
                                    uint32_t nbins, uint32_t* flags, int sms,
@@ -128,6 +134,7 @@ struct ecc_ctx {
   PinBuf staging[2];
   PinBuf host_small;
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
+  DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
 
@@ -507,7 +514,7 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
-                    &ctx->fused, &ctx->bscratch})
+                    &ctx->fused, &ctx->bscratch, &ctx->nanidx})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -643,11 +650,18 @@ int ecc_curve(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype, ecc_di
                        n_out, true);
 }
 
-int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
+// Raw-file fixups done on the device right after each chunk's H2D
+// (image.hpp:39-52): byte swap of big-endian f32 and NaN rejection.
+struct Fixup {
+  bool active = false;
+  bool big_endian = false;
+};
+
+static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
                        ecc_dtype dtype, ecc_dims dims, const uint64_t* bounds,
                        size_t nchunks, const ecc_binmap* bm, ecc_chunk_timing* timings,
                        void* values_out, int64_t* changes_out, uint64_t cap,
-                       uint64_t* n_out) {
+                       uint64_t* n_out, Fixup fix) {
   CKI(bind(ctx));
   CKI(check_dtype(dtype));
   if (dims.w0 < 1) return fail(ECC_EINVAL, "w0 must be >= 1");
@@ -696,6 +710,10 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     CKR(cudaEventCreate(&used[b]));
     CKR(cudaEventCreate(&kb[b]));
     CKR(cudaEventCreate(&ke[b]));
+  }
+  if (fix.active) {
+    CKI(ctx->nanidx.ensure(8 * nchunks));
+    CKR(cudaMemsetAsync(ctx->nanidx.p, 0xFF, 8 * nchunks, st));
   }
   CKR(cudaEventRecord(ev0, st));
   // map device event times onto the host clock of the ChunkTiming fields
@@ -751,6 +769,12 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     CKI(harvest(b));
     CKR(cudaStreamWaitEvent(st, h2d_done[b], 0));
     CKR(cudaEventRecord(kb[b], st));
+    if (fix.active) {
+      CKR(launch_fixup(ctx->slab[b].p, (int)dtype, (r1 - r0) * dims.w1 * dims.w2,
+                       r0 * dims.w1 * dims.w2, fix.big_endian,
+                       ctx->nanidx.as<unsigned long long>() + k, ctx->sms, st));
+      ctx->launches += 1;
+    }
     const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
     t.merge_begin = since();
     if (sorted) {
@@ -775,6 +799,15 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   }
   cudaEventDestroy(ev0);
   if (rc != ECC_OK) return rc;
+  if (fix.active) {  // the first chunk (in plan order) whose rows held a NaN
+    std::vector<unsigned long long> nan(nchunks);
+    CKR(cudaMemcpyAsync(nan.data(), ctx->nanidx.p, 8 * nchunks, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+    for (size_t k = 0; k < nchunks; ++k)
+      if (nan[k] != ~0ull)
+        return fail(ECC_ESOURCE, "ingestion of chunk " + std::to_string(k) +
+                                     " failed: NaN value at linear index " + std::to_string(nan[k]));
+  }
   BinResult r;
   if (sorted) {
     CKI(read_flags(ctx, st));
@@ -795,6 +828,76 @@ int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   write_values(dtype, sorted, am, r, values_out);
   std::memcpy(changes_out, r.changes.data(), m * 8);
   return ECC_OK;
+}
+
+int ecc_process_stream(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
+                       ecc_dtype dtype, ecc_dims dims, const uint64_t* bounds,
+                       size_t nchunks, const ecc_binmap* bm, ecc_chunk_timing* timings,
+                       void* values_out, int64_t* changes_out, uint64_t cap,
+                       uint64_t* n_out) {
+  return stream_impl(ctx, read_rows, user, dtype, dims, bounds, nchunks, bm, timings, values_out,
+                     changes_out, cap, n_out, Fixup{});
+}
+
+namespace {
+struct FileReader {
+  int fd = -1;
+  std::string path;
+  uint64_t row_bytes = 0;
+};
+
+int file_read_rows(void* user, uint64_t r0, uint64_t r1, void* dst, char* errbuf,
+                   size_t errlen) {
+  auto* f = static_cast<FileReader*>(user);
+  uint64_t off = r0 * f->row_bytes, left = (r1 - r0) * f->row_bytes;
+  char* p = static_cast<char*>(dst);
+  while (left) {
+    const ssize_t n = pread(f->fd, p, std::min<uint64_t>(left, 1ull << 30), (off_t)off);
+    if (n <= 0) {
+      std::snprintf(errbuf, errlen, "read failure on '%s' at row %llu", f->path.c_str(),
+                    (unsigned long long)r0);
+      return 1;
+    }
+    p += n;
+    off += (uint64_t)n;
+    left -= (uint64_t)n;
+  }
+  return 0;
+}
+}  // namespace
+
+int ecc_process_file(ecc_ctx* ctx, const char* path, ecc_dtype dtype, ecc_dims dims,
+                     int big_endian, const uint64_t* bounds, size_t nchunks,
+                     const ecc_binmap* bm, ecc_chunk_timing* timings, void* values_out,
+                     int64_t* changes_out, uint64_t cap, uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_dims(dims));
+  if (!path) return fail(ECC_EINVAL, "null path");
+  FileReader f;
+  f.path = path;
+  f.row_bytes = dims.w1 * dims.w2 * esize(dtype);
+  f.fd = open(path, O_RDONLY);
+  if (f.fd < 0) return fail(ECC_ESOURCE, std::string("cannot open '") + path + "'");
+  struct stat stt;
+  const uint64_t expected = dims.w0 * f.row_bytes;
+  if (fstat(f.fd, &stt) != 0) {
+    close(f.fd);
+    return fail(ECC_ESOURCE, std::string("cannot stat '") + path + "'");
+  }
+  if ((uint64_t)stt.st_size != expected) {
+    close(f.fd);
+    return fail(ECC_EINVAL, std::string("size mismatch for '") + path + "': expected " +
+                                std::to_string(expected) + " bytes for dims " + dims_str(dims) +
+                                ", found " + std::to_string((uint64_t)stt.st_size));
+  }
+  Fixup fix;
+  fix.active = dtype == ECC_F32;  // u8 / u16 files need neither swap nor NaN check
+  fix.big_endian = big_endian != 0;
+  const int rc = stream_impl(ctx, file_read_rows, &f, dtype, dims, bounds, nchunks, bm, timings,
+                             values_out, changes_out, cap, n_out, fix);
+  close(f.fd);
+  return rc;
 }
 
 int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims dims,

@@ -324,6 +324,31 @@ cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- raw-file fixups
+// image.hpp:39-52 on the device: big-endian f32 byte swap in place and the
+// smallest linear index of a NaN (atomicMin; ~0 when there is none).
+__global__ void k_fixup_f32(uint32_t* d, uint64_t n, uint64_t base, bool swap,
+                            unsigned long long* nan_min) {
+  unsigned long long first = ~0ull;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t u = d[i];
+    if (swap) {
+      u = __byte_perm(u, 0, 0x0123);
+      d[i] = u;
+    }
+    if ((u & 0x7F800000u) == 0x7F800000u && (u & 0x007FFFFFu) && first == ~0ull) first = base + i;
+  }
+  if (first != ~0ull) atomicMin(nan_min, first);
+}
+
+cudaError_t launch_fixup(void* d, int dtype, uint64_t n, uint64_t base, bool big_endian,
+                         unsigned long long* nan_min, int sms, cudaStream_t st) {
+  if (dtype != 2) return cudaSuccess;
+  k_fixup_f32<<<sms * 8, 256, 0, st>>>(static_cast<uint32_t*>(d), n, base, big_endian, nan_min);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- inputs
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <random>
 #include <string>
 #include <vector>
@@ -317,6 +318,45 @@ TEST_GPU("engine report has one timing per chunk") {
   CHECK(v.total() == 1);
   CHECK(rep.chunks.size() == 4);
   for (const auto& t : rep.chunks) CHECK(t.kernel_end >= t.kernel_begin);
+} END_TEST
+
+TEST_GPU("FileSource: raw f32 little / big endian, NaN and size errors (chunk.hpp:154-189)") {
+  std::mt19937 rng(21);
+  const Dims d{9, 7, 5};
+  std::vector<float> v(d.voxel_count());
+  for (auto& x : v) x = float(rng() % 7) * 0.5f;
+  Image<float> img{d, v};
+  const std::string le = "/tmp/ecc_test_le.raw", be = "/tmp/ecc_test_be.raw";
+  {
+    std::FILE* f = std::fopen(le.c_str(), "wb");
+    std::fwrite(v.data(), 4, v.size(), f);
+    std::fclose(f);
+    f = std::fopen(be.c_str(), "wb");
+    for (float x : v) {
+      uint32_t u;
+      std::memcpy(&u, &x, 4);
+      u = __builtin_bswap32(u);
+      std::fwrite(&u, 4, 1, f);
+    }
+    std::fclose(f);
+  }
+  const auto plan = plan_chunks<float>(d, ChunkTarget::count(3));
+  FileSource<float> a(le, d), b(be, d, RawOptions{true});
+  CHECK(same(process_image(a, plan), oracle_vcec(img)));
+  CHECK(same(process_image(b, plan), oracle_vcec(img)));
+  FileSource<float> wrong(le, Dims{9, 7, 4});
+  CHECK_THROWS_WITH(process_image(wrong, plan_chunks<float>(Dims{9, 7, 4}, ChunkTarget::count(2))),
+                    "size mismatch");
+  v[(5 * 7 + 1) * 5 + 2] = std::numeric_limits<float>::quiet_NaN();
+  {
+    std::FILE* f = std::fopen(le.c_str(), "wb");
+    std::fwrite(v.data(), 4, v.size(), f);
+    std::fclose(f);
+  }
+  FileSource<float> nan(le, d);
+  CHECK_THROWS_WITH(process_image(nan, plan), "NaN value at linear index 182");
+  std::remove(le.c_str());
+  std::remove(be.c_str());
 } END_TEST
 
 int main(int argc, char** argv) {

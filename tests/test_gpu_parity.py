@@ -293,3 +293,41 @@ def test_config4_golden_device_resident(ctx, golden):
     c = ctx.curve(vol, binmap=eb.quantised_binmap(65536))
     assert oracle.curve_digest(c.thresholds, c.chi) == golden["configs"]["C4"]["digest"]
     assert c.size() == 65536 and int(c.chi[-1]) == 1
+
+
+def test_process_file_raw_and_big_endian(ctx, tmp_path):
+    """FileSource semantics (chunk.hpp:154-189, image.hpp:39-52) with the f32
+    byte swap and NaN check on the GPU; error wording as the reference."""
+    rng = np.random.default_rng(12)
+    img = rng.random((9, 7, 5)).astype(np.float32)
+    img[3, 2, 1] = -0.0
+    dims = eb.Dims.of(img.shape)
+    plan = eb.plan_chunks(dims, eb.ChunkTarget.count(3))
+    want = oracle.vcec(img)
+    le, be = tmp_path / "le.raw", tmp_path / "be.raw"
+    img.tofile(le)
+    img.astype(">f4").tofile(be)
+    for path, big in ((le, False), (be, True)):
+        got = ctx.process_file(str(path), dims, np.float32, plan, big_endian=big)
+        assert _same(got.values, got.changes, *want), path
+    u8 = rng.integers(0, 256, (12, 16, 32)).astype(np.uint8)
+    p8 = tmp_path / "u8.raw"
+    u8.tofile(p8)
+    got = ctx.process_file(str(p8), eb.Dims.of(u8.shape), np.uint8,
+                           eb.plan_chunks(eb.Dims.of(u8.shape), eb.ChunkTarget.count(4)))
+    assert _same(got.values, got.changes, *oracle.vcec(u8))
+    # NaN: first chunk (in plan order) whose rows hold one, reference wording
+    bad = img.copy()
+    bad[5, 1, 2] = np.nan
+    pb = tmp_path / "nan.raw"
+    bad.tofile(pb)
+    with pytest.raises(eb.EccError) as ei:
+        ctx.process_file(str(pb), dims, np.float32, plan)
+    idx = (5 * 7 + 1) * 5 + 2
+    assert f"NaN value at linear index {idx}" in str(ei.value) and "chunk" in str(ei.value)
+    with pytest.raises(eb.EccError) as ei:
+        ctx.process_file(str(le), eb.Dims(9, 7, 4), np.float32)
+    assert "size mismatch" in str(ei.value)
+    with pytest.raises(eb.EccError) as ei:
+        ctx.process_file(str(tmp_path / "missing.raw"), dims, np.float32)
+    assert "cannot open" in str(ei.value)
