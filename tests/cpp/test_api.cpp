@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <sstream>
 #include <limits>
 #include <random>
 #include <string>
@@ -359,8 +360,44 @@ TEST_GPU("FileSource: raw f32 little / big endian, NaN and size errors (chunk.hp
   std::remove(be.c_str());
 } END_TEST
 
+// `test_api csv <file>`: file = u64 n, n float32 thresholds, n int64 chi;
+// writes the curve CSV (tests/test_native.py compares it with the
+// reference's own writer).
+static int csv_mode(const char* path) {
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) return 2;
+  std::uint64_t n = 0;
+  if (std::fread(&n, 8, 1, f) != 1) return 2;
+  EccCurve<float> c;
+  c.thresholds.resize(n);
+  c.chi.resize(n);
+  if (std::fread(c.thresholds.data(), 4, n, f) != n || std::fread(c.chi.data(), 8, n, f) != n) return 2;
+  std::fclose(f);
+  std::ostringstream os;
+  write_curve(c, CurveFormat::csv, os);
+  std::fwrite(os.str().data(), 1, os.str().size(), stdout);
+  return 0;
+}
+
+TEST_CPU("curve writers: CSV / JSON / VCEC layouts and round trip") {
+  EccCurve<float> c{{0.0f, 1.5258789e-05f, 0.5f, 1e10f}, {3, -2, 0, 1}};
+  std::ostringstream csv, json, vc;
+  write_curve(c, CurveFormat::csv, csv);
+  write_curve(c, CurveFormat::json, json);
+  CHECK(csv.str() == "threshold,euler_characteristic\n0,3\n1.5258789e-05,-2\n0.5,0\n1e+10,1\n");
+  CHECK(json.str() == "[{\"t\":0,\"chi\":3},{\"t\":1.5258789e-05,\"chi\":-2},{\"t\":0.5,\"chi\":0},"
+                      "{\"t\":1e+10,\"chi\":1}]\n");
+  std::istringstream in(csv.str());
+  CHECK(read_curve_csv<float>(in) == c);
+  write_vcec(GlobalVcec<std::uint8_t>{{0, 9}, {0, 1}}, vc);
+  CHECK(vc.str() == "value,change\n0,0\n9,1\n");
+  std::istringstream bad("threshold,chi\n");
+  CHECK_THROWS_WITH(read_curve_csv<float>(bad), "bad curve CSV header");
+} END_TEST
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "cpu";
+  if (mode == "csv" && argc > 2) return csv_mode(argv[2]);
   int ran = 0;
   for (auto& c : registry()) {
     if (c.gpu != (mode == "gpu")) continue;

@@ -46,3 +46,27 @@ def test_cpp_headers_compile_standalone(tmp_path):
 def test_cpp_api_gpu_cases():
     out = _run([_bin("test_api"), "gpu"])
     assert "0 failures" in out, out
+
+
+def test_cpp_curve_csv_matches_reference_writer(tmp_path):
+    """include/ecc/curve.hpp write_curve vs the reference's own write_curve
+    (compiled in oracle/_ref): byte-identical CSV for float thresholds,
+    including the shortest round-trip formatting of awkward values."""
+    import numpy as np
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("reference not compiled here")
+    rng = np.random.default_rng(3)
+    t = np.unique(np.concatenate([
+        rng.random(500).astype(np.float32),
+        (rng.integers(0, 65536, 300) * 2.0 ** -16).astype(np.float32),
+        np.array([0.0, 1e-38, 3.4e38, 1e10, 123456.7, 2.0 ** -149, 0.1, 1.0 / 3], np.float32),
+        -rng.random(50).astype(np.float32) * 1e6]))
+    chi = rng.integers(-10 ** 12, 10 ** 12, t.size).astype(np.int64)
+    f = tmp_path / "c.bin"
+    with open(f, "wb") as fh:
+        fh.write(np.uint64(t.size).tobytes())
+        fh.write(t.astype(np.float32).tobytes())
+        fh.write(chi.tobytes())
+    mine = subprocess.run([_bin("test_api"), "csv", str(f)], capture_output=True, check=True).stdout
+    assert mine == oracle.ref_csv(t, chi)
