@@ -134,6 +134,7 @@ struct ecc_ctx {
   PinBuf staging[2];
   PinBuf host_small;
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
+  DevBuf pad;       // row-padded copy of a u8 slab for the TMA kernel
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
@@ -234,8 +235,31 @@ int read_flags(ecc_ctx* ctx, cudaStream_t st) {
 
 // Accumulate one slab into ctx->hist (already zeroed), dispatching to the
 // specialised kernels when they cover the shape.
-int accumulate(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine,
+// 3D u8 slabs whose rows are not a multiple of 16 bytes (TMA stride rule)
+// or whose base is not 16-byte aligned are copied once into a padded
+// device buffer (row pitch rounded up to 16) so they too take the
+// bit-sliced kernel; the padding columns lie outside w2 and read as collar.
+int pad_for_u8_fast(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine, cudaStream_t st,
+                    Slab* out) {
+  *out = s;
+  if (dtype != ECC_U8 || affine || s.w2 <= 1 || u8_3d_supported(s)) return ECC_OK;
+  Slab p = s;
+  p.pitch = (s.w2 + 15) / 16 * 16;
+  if (!u8_3d_supported(Slab{nullptr, p.plane0, p.nplanes, p.w0, p.w1, p.w2, p.own0, p.own1,
+                            p.pitch}))
+    return ECC_OK;  // too large for the fast path: stays on the generic kernel
+  CKI(ctx->pad.ensure((size_t)s.nplanes * s.w1 * p.pitch));
+  CKR(cudaMemcpy2DAsync(ctx->pad.p, (size_t)p.pitch, s.base, (size_t)s.row_pitch(), (size_t)s.w2,
+                        (size_t)(s.nplanes * s.w1), cudaMemcpyDeviceToDevice, st));
+  p.base = ctx->pad.p;
+  *out = p;
+  return ECC_OK;
+}
+
+int accumulate(ecc_ctx* ctx, const Slab& s0, ecc_dtype dtype, bool affine,
                const AffineMap& am, uint32_t nbins, int64_t* hist, cudaStream_t st) {
+  Slab s;
+  CKI(pad_for_u8_fast(ctx, s0, dtype, affine, st, &s));
   bool handled = false;
   CKR(launch_accumulate_fast(s, (int)dtype, affine, am, hist, nbins,
                              ctx->flags.as<uint32_t>(), ctx->sms, st, &handled));
@@ -434,7 +458,10 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
     merge_runs(keys, sums, {0, keys.size()}, res);
     return ECC_OK;
   }
-  if (fusable(dtype, s, affine)) {
+  Slab sp;
+  CKI(pad_for_u8_fast(ctx, s, dtype, affine, st, &sp));
+  if (fusable(dtype, sp, affine)) {
+    const Slab& s = sp;
     CKI(ctx->bins.ensure(nbins * 4ull));
     CKI(ctx->changes.ensure(nbins * 8ull));
     CKI(ctx->chi.ensure(nbins * 8ull));
@@ -514,7 +541,7 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
-                    &ctx->fused, &ctx->bscratch, &ctx->nanidx})
+                    &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -587,7 +614,9 @@ int ecc_curve_device(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims
   if (sorted) return fail(ECC_EINVAL, "the sorted bin map has no device-side curve; use ecc_curve");
   cudaStream_t st = pick(ctx, stream);
   const Slab s = make_slab(d_data, dims, 0, dims.w0, 0, dims.w0);
-  if (fusable(dtype, s, affine)) return launch_fused(ctx, s, d_bins, d_changes, d_chi, d_count, st);
+  Slab sp;
+  CKI(pad_for_u8_fast(ctx, s, dtype, affine, st, &sp));
+  if (fusable(dtype, sp, affine)) return launch_fused(ctx, sp, d_bins, d_changes, d_chi, d_count, st);
   CKI(ctx->flags.ensure(4));
   CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
   CKI(ctx->hist.ensure(2 * nbins * 8));

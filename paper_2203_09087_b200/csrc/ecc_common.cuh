@@ -143,6 +143,8 @@ struct Slab {
   int64_t plane0, nplanes;
   int64_t w0, w1, w2;
   int64_t own0, own1;
+  int64_t pitch = 0;  // elements between consecutive rows in memory (0 = w2)
+  __host__ __device__ int64_t row_pitch() const { return pitch ? pitch : w2; }
 };
 
 }  // namespace eccb

@@ -477,7 +477,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // stride rule), 16-byte aligned slab base, and per-CTA voxel counts that fit
 // the 32-bit shared counters.
 bool u8_3d_supported(const Slab& s) {
-  return s.w2 > 1 && s.w2 % 16 == 0 && (reinterpret_cast<uintptr_t>(s.base) % 16) == 0 &&
+  return s.w2 > 1 && s.row_pitch() % 16 == 0 && (reinterpret_cast<uintptr_t>(s.base) % 16) == 0 &&
          s.w1 <= (1 << 30) && s.w2 <= (1 << 30) && s.w0 <= (1 << 30) &&
          (s.own1 - s.own0) * s.w1 * s.w2 < (1ll << 40);
 }
@@ -489,14 +489,15 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   // is host work on every call otherwise)
   thread_local struct {
     const void* base = nullptr;
-    int64_t w1 = 0, w2 = 0, np = 0;
+    int64_t w1 = 0, w2 = 0, np = 0, pitch = 0;
     CUtensorMap map;
   } cache;
-  if (cache.base != s.base || cache.w1 != s.w1 || cache.w2 != s.w2 || cache.np != s.nplanes) {
+  if (cache.base != s.base || cache.w1 != s.w1 || cache.w2 != s.w2 || cache.np != s.nplanes ||
+      cache.pitch != s.row_pitch()) {
     auto enc = encode_fn();
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[3] = {(cuuint64_t)s.w2, (cuuint64_t)s.w1, (cuuint64_t)s.nplanes};
-    const cuuint64_t strides[2] = {(cuuint64_t)s.w2, (cuuint64_t)(s.w1 * s.w2)};
+    const cuuint64_t strides[2] = {(cuuint64_t)s.row_pitch(), (cuuint64_t)(s.w1 * s.row_pitch())};
     const cuuint32_t box[3] = {BOXZ, BOXY, 1};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&cache.map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(s.base), dims,
@@ -510,6 +511,7 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
     cache.w1 = s.w1;
     cache.w2 = s.w2;
     cache.np = s.nplanes;
+    cache.pitch = s.row_pitch();
   }
   const CUtensorMap& map = cache.map;
   Geom g;

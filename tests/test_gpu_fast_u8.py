@@ -114,3 +114,20 @@ def test_sharded_driver_on_one_gpu(ctx, world):
     assert np.array_equal(bins[:m].cpu().numpy(), v.astype(np.int32))
     assert np.array_equal(chg[:m].cpu().numpy(), c)
     assert np.array_equal(chi[:m].cpu().numpy(), np.cumsum(c))
+
+
+@pytest.mark.parametrize("shape", [(40, 50, 77), (9, 33, 100), (5, 7, 3), (3, 300, 17), (17, 16, 129)])
+def test_odd_row_widths_take_the_padded_fast_path(ctx, shape):
+    """Rows that are not a multiple of 16 bytes (or a misaligned base) are
+    copied once into a 16-byte row pitch and run through the TMA kernel."""
+    import torch
+    rng = np.random.default_rng(sum(shape) + 1)
+    img = rng.integers(0, 256, shape).astype(np.uint8)
+    _check(ctx, img)
+    # misaligned device base: a view starting one byte into a buffer
+    flat = torch.empty(img.size + 1, dtype=torch.uint8, device="cuda")
+    flat[1:].copy_(torch.from_numpy(img.ravel()))
+    dev = flat[1:].view(shape)
+    got = ctx.vcec(dev)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(got.changes, c)
