@@ -331,3 +331,70 @@ def test_process_file_raw_and_big_endian(ctx, tmp_path):
     with pytest.raises(eb.EccError) as ei:
         ctx.process_file(str(tmp_path / "missing.raw"), dims, np.float32)
     assert "cannot open" in str(ei.value)
+
+
+def test_acceptance_sweep_1000_images(ctx):
+    """acceptance.cpp:95-142: 1000 random images (dims {1..8}^2 and {1..6}^3,
+    u8 values 0..7, f32 drawn from a pool of 5 values), every chunking in
+    {1, 2, 3, w0}, equal to the oracle."""
+    rng = np.random.default_rng(2024)
+    pool = np.array([-1.5, 0.0, 0.25, 3.0, 7.5], np.float32)
+    for t in range(1000):
+        d = (tuple(int(x) for x in rng.integers(1, 9, 2)) if t % 2 == 0 else
+             tuple(int(x) for x in rng.integers(1, 7, 3)))
+        img = (rng.integers(0, 8, d).astype(np.uint8) if t % 4 < 2 else
+               pool[rng.integers(0, 5, d)])
+        want = oracle.vcec(img)
+        cs = {1, 2, 3, img.shape[0]} if t % 10 == 0 else {1 + t % 3}
+        for c in sorted(cs):
+            plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(c))
+            got = eb.process_image(img, plan)
+            assert _same(got.values, got.changes, *want), (t, img.shape, c)
+
+
+def test_order_only_dependence(ctx):
+    """test_kernel.cpp:175-200: only the order of values matters -- a strictly
+    increasing remap leaves every change unchanged."""
+    rng = np.random.default_rng(31)
+    for shape in [(20, 30, 40), (64, 64, 1), (9, 16, 48)]:
+        img = rng.integers(0, 256, shape).astype(np.uint8)
+        a = ctx.vcec(img)
+        f = (img.astype(np.float32) * 0.5 - 3.0).astype(np.float32)
+        b = ctx.vcec(f)
+        u = (img.astype(np.uint16) * 200 + 7).astype(np.uint16)
+        c = ctx.vcec(u)
+        assert np.array_equal(a.changes, b.changes) and np.array_equal(a.changes, c.changes)
+
+
+def test_chunk_invariance_64_cubed_bitwise(ctx):
+    """acceptance.cpp:203-227: bitwise-identical curves over chunk counts
+    1..8 on 64^3 (u8 through the fast path, f32 through the sorted path)."""
+    rng = np.random.default_rng(64)
+    u8 = rng.integers(0, 256, (64, 64, 64)).astype(np.uint8)
+    f32 = rng.integers(0, 40, (64, 64, 64)).astype(np.float32) * np.float32(0.125)
+    for img in (u8, f32):
+        ref = None
+        for c in range(1, 9):
+            plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(c))
+            v = eb.process_image(img, plan)
+            cur = eb.vcec_to_ecc(v)
+            key = (cur.thresholds.tobytes(), cur.chi.tobytes())
+            ref = ref or key
+            assert key == ref, c
+        assert np.array_equal(v.changes, oracle.vcec(img)[1])
+
+
+def test_memory_budget_plan_streams_out_of_core_shape(ctx):
+    """acceptance.cpp:253-290: a 1024 x 256^2 f32 volume planned under a
+    64 MiB budget streams chunk by chunk and matches the whole-volume result."""
+    rng = np.random.default_rng(5)
+    img = (rng.integers(0, 1000, (1024, 256, 256)).astype(np.float32) * np.float32(0.001))
+    dims = eb.Dims.of(img.shape)
+    plan = eb.plan_chunks(dims, eb.ChunkTarget.memory_budget(64 << 20), dtype=np.float32)
+    assert plan.chunk_count() > 8
+    for r in plan.ranges:
+        assert eb.padded_chunk_bytes(dims, r.len(), np.float32) <= 64 << 20
+    v = eb.process_image(img, plan)
+    assert v.total() == 1
+    q = ctx.vcec(img)
+    assert np.array_equal(v.changes, q.changes)
