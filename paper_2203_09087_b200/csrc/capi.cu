@@ -6,6 +6,7 @@
 // work happens in the kernels; there is no host compute path.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -135,6 +136,8 @@ struct ecc_ctx {
   PinBuf host_small;
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
   DevBuf pad;       // row-padded copy of a u8 slab for the TMA kernel
+  DevBuf finscr;    // K3 partials for large bin counts
+  DevBuf keys16;    // 16-bit keys (u16 padded / f32 bin indices) for k_u16_3d
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
@@ -190,6 +193,13 @@ int resolve_bins(ecc_dtype dtype, const ecc_binmap* bm, uint64_t* nbins,
   am->step = bm->step;
   am->inv_step = 1.0 / (double)bm->step;
   am->nbins = bm->nbins;
+  am->pow2_scale = 0.0f;
+  {
+    int e = 0;
+    const double mant = std::frexp((double)bm->step, &e);
+    if (bm->lo == 0.0f && mant == 0.5 && e <= 1 && e > -100 && bm->nbins <= (1u << 22))
+      am->pow2_scale = (float)(1.0 / (double)bm->step);
+  }
   return ECC_OK;
 }
 
@@ -256,8 +266,47 @@ int pad_for_u8_fast(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine, c
   return ECC_OK;
 }
 
+// 3D u16 volumes and affine-quantised f32 volumes with <= 65536 bins run the
+// 16-bit bit-sliced kernel (k_u16_3d.cu): f32 slabs are first mapped to bin
+// indices (monotone, so the stencil sees the same order), u16 slabs whose
+// rows break the 16-byte TMA stride rule are copied to a padded pitch.
+int accumulate_keys16(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine,
+                      const AffineMap& am, uint32_t nbins, int64_t* hist, cudaStream_t st,
+                      bool* handled) {
+  *handled = false;
+  const bool u16 = dtype == ECC_U16 && !affine && nbins == 65536;
+  const bool f32 = dtype == ECC_F32 && affine && nbins <= 65536;
+  if (s.w2 <= 1 || !(u16 || f32) || s.w1 > (1 << 30) || s.w2 > (1 << 30) || s.w0 > (1 << 30))
+    return ECC_OK;
+  Slab k = s;
+  if (f32 || !u16_3d_supported(s)) {
+    k.pitch = (s.w2 + 7) / 8 * 8;
+    CKI(ctx->keys16.ensure((size_t)s.nplanes * s.w1 * k.pitch * 2));
+    if (f32) {
+      CKR(launch_affine_keys(static_cast<const float*>(s.base), (uint64_t)(s.nplanes * s.w1),
+                             (uint32_t)s.w2, (uint32_t)k.pitch, am, ctx->keys16.as<uint16_t>(),
+                             ctx->flags.as<uint32_t>(), ctx->sms, st));
+      ctx->launches += 1;
+    } else {
+      CKR(cudaMemcpy2DAsync(ctx->keys16.p, (size_t)k.pitch * 2, s.base, (size_t)s.row_pitch() * 2,
+                            (size_t)s.w2 * 2, (size_t)(s.nplanes * s.w1),
+                            cudaMemcpyDeviceToDevice, st));
+    }
+    k.base = ctx->keys16.p;
+  }
+  CKR(launch_u16_3d(k, nbins, hist, ctx->sms, st));
+  ctx->launches += 1;
+  *handled = true;
+  return ECC_OK;
+}
+
 int accumulate(ecc_ctx* ctx, const Slab& s0, ecc_dtype dtype, bool affine,
                const AffineMap& am, uint32_t nbins, int64_t* hist, cudaStream_t st) {
+  {
+    bool done = false;
+    CKI(accumulate_keys16(ctx, s0, dtype, affine, am, nbins, hist, st, &done));
+    if (done) return ECC_OK;
+  }
   Slab s;
   CKI(pad_for_u8_fast(ctx, s0, dtype, affine, st, &s));
   bool handled = false;
@@ -317,9 +366,10 @@ int finalize_to_host(ecc_ctx* ctx, uint32_t nbins, cudaStream_t st, BinResult* o
   CKI(ctx->changes.ensure(nbins * 8ull));
   CKI(ctx->chi.ensure(nbins * 8ull));
   CKI(ctx->count.ensure(8));
+  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
   CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, ctx->bins.as<uint32_t>(),
                       ctx->changes.as<int64_t>(), ctx->chi.as<int64_t>(),
-                      ctx->count.as<uint64_t>(), st));
+                      ctx->count.as<uint64_t>(), ctx->finscr.p, st));
   ctx->launches += 1;
   uint64_t m = 0;
   CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
@@ -541,7 +591,8 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
-                    &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad})
+                    &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad,
+                    &ctx->keys16, &ctx->finscr})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -622,8 +673,9 @@ int ecc_curve_device(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims
   CKI(ctx->hist.ensure(2 * nbins * 8));
   CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
   CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
+  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
   CKR(launch_finalize(ctx->hist.as<int64_t>(), (uint32_t)nbins, d_bins, d_changes, d_chi, d_count,
-                      st));
+                      ctx->finscr.p, st));
   ctx->launches += 1;
   if (affine) CKI(read_flags(ctx, st));
   return ECC_OK;
@@ -635,7 +687,8 @@ int ecc_finalize(ecc_ctx* ctx, const int64_t* d_hist, uint64_t nbins, uint32_t* 
   if (!d_hist || !d_bins || !d_changes || !d_chi || !d_count)
     return fail(ECC_EINVAL, "null device pointer");
   if (nbins < 1 || nbins > (1u << 24)) return fail(ECC_EINVAL, "bad bin count");
-  CKR(launch_finalize(d_hist, (uint32_t)nbins, d_bins, d_changes, d_chi, d_count,
+  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
+  CKR(launch_finalize(d_hist, (uint32_t)nbins, d_bins, d_changes, d_chi, d_count, ctx->finscr.p,
                       pick(ctx, stream)));
   ctx->launches += 1;
   return ECC_OK;

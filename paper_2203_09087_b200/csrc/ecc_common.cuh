@@ -107,6 +107,7 @@ struct AffineMap {
   float lo, step;
   double inv_step;
   uint32_t nbins;
+  float pow2_scale;  // 1/step when lo == 0 and step is a power of two, else 0
 };
 
 __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,
@@ -122,6 +123,18 @@ __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,
 
 __device__ __forceinline__ uint32_t affine_bin(const AffineMap& m, float v,
                                                uint32_t* flags) {
+  if (m.pow2_scale != 0.0f) {
+    // lo = 0, step = 2^-k: v * 2^k is exact, and v is on the grid iff that
+    // product is an integer (2^23 magic rounding); same accepted set and
+    // bins as the double-precision check below (BASELINE config 4's grid).
+    const float t = v * m.pow2_scale;
+    if (t >= 0.0f && t < (float)m.nbins) {
+      const float mg = t + 8388608.0f;
+      if (mg - 8388608.0f == t) return __float_as_uint(mg) - 0x4B000000u;
+    }
+    atomicOr(flags, v != v ? kFlagNaN : kFlagBinmap);
+    return 0;
+  }
   const double t = __dmul_rn(__dadd_rn((double)v, -(double)m.lo), m.inv_step);
   const double r = rint(t);
   uint32_t bin = 0;

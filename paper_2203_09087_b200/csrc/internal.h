@@ -20,6 +20,11 @@ struct U83dFinalize {
   uint64_t* count;
 };
 bool u8_3d_supported(const Slab& s);
+bool u16_3d_supported(const Slab& s);
+cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms, cudaStream_t st);
+cudaError_t launch_affine_keys(const float* v, uint64_t rows, uint32_t w2, uint32_t pitch,
+                               const AffineMap& am, uint16_t* keys, uint32_t* flags, int sms,
+                               cudaStream_t st);
 cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cudaStream_t st,
                          const U83dFinalize* fz = nullptr);
 
@@ -31,8 +36,10 @@ cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sm
                                    cudaStream_t st);
 cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys,
                               uint32_t* flags, int sms, cudaStream_t st);
+// K3; `scratch` (16 bytes per 1024 bins) enables the multi-CTA version for
+// large bin counts.
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
-                            int64_t* changes, int64_t* chi, uint64_t* count,
+                            int64_t* changes, int64_t* chi, uint64_t* count, void* scratch,
                             cudaStream_t st);
 cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
                         uint64_t base, int sms, cudaStream_t st);

@@ -317,10 +317,97 @@ __global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ h
   if (threadIdx.x == 1023) *count = (uint64_t)total.x;
 }
 
+// Large bin counts (65536 for u16 / quantised f32): three small grids --
+// per-1024-bin partial (count, sum), one scan of the partials, and the
+// block-local scan that writes the compacted curve -- instead of one CTA
+// walking all bins.
+namespace fin {
+constexpr int T = 256, PER = 4, B = T * PER;
+
+struct Add2 {
+  __device__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+    return make_longlong2(a.x + b.x, a.y + b.y);
+  }
+};
+
+__global__ void __launch_bounds__(T) k_partials(const int64_t* __restrict__ hist, uint32_t nbins,
+                                                longlong2* __restrict__ part) {
+  using Red = cub::BlockReduce<longlong2, T>;
+  __shared__ typename Red::TempStorage tmp;
+  const uint32_t b0 = blockIdx.x * B + threadIdx.x * PER;
+  longlong2 v = make_longlong2(0, 0);
+#pragma unroll
+  for (int i = 0; i < PER; ++i)
+    if (b0 + i < nbins) {
+      v.x += hist[nbins + b0 + i] != 0;
+      v.y += hist[b0 + i];
+    }
+  const longlong2 t = Red(tmp).Reduce(v, Add2());
+  if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_partials(longlong2* part, uint32_t nblk,
+                                                        uint64_t* count) {
+  using Scan = cub::BlockScan<longlong2, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const uint32_t per = (nblk + 1023) / 1024;
+  const uint32_t a = min(nblk, threadIdx.x * per), b = min(nblk, a + per);
+  longlong2 loc = make_longlong2(0, 0);
+  for (uint32_t j = a; j < b; ++j) loc = Add2()(loc, part[j]);
+  longlong2 ex, total;
+  Scan(tmp).ExclusiveScan(loc, ex, make_longlong2(0, 0), Add2(), total);
+  for (uint32_t j = a; j < b; ++j) {
+    const longlong2 p = part[j];
+    part[j] = ex;
+    ex = Add2()(ex, p);
+  }
+  if (threadIdx.x == 0) *count = (uint64_t)total.x;
+}
+
+__global__ void __launch_bounds__(T) k_write(const int64_t* __restrict__ hist, uint32_t nbins,
+                                             const longlong2* __restrict__ part, uint32_t* bins,
+                                             int64_t* changes, int64_t* chi) {
+  using Scan = cub::BlockScan<longlong2, T>;
+  __shared__ typename Scan::TempStorage tmp;
+  const uint32_t b0 = blockIdx.x * B + threadIdx.x * PER;
+  int64_t s[PER], n[PER];
+  longlong2 v = make_longlong2(0, 0);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const bool in = b0 + i < nbins;
+    s[i] = in ? hist[b0 + i] : 0;
+    n[i] = in ? hist[nbins + b0 + i] : 0;
+    v.x += n[i] != 0;
+    v.y += s[i];
+  }
+  longlong2 ex;
+  Scan(tmp).ExclusiveScan(v, ex, make_longlong2(0, 0), Add2());
+  long long pos = part[blockIdx.x].x + ex.x, acc = part[blockIdx.x].y + ex.y;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    acc += s[i];
+    if (n[i] != 0) {
+      bins[pos] = b0 + i;
+      changes[pos] = s[i];
+      chi[pos] = acc;
+      ++pos;
+    }
+  }
+}
+}  // namespace fin
+
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
-                            int64_t* changes, int64_t* chi, uint64_t* count,
+                            int64_t* changes, int64_t* chi, uint64_t* count, void* scratch,
                             cudaStream_t st) {
-  k_finalize<<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
+  if (nbins <= 4096 || !scratch) {
+    k_finalize<<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
+    return cudaGetLastError();
+  }
+  const uint32_t nblk = (nbins + fin::B - 1) / fin::B;  // scratch: nblk x 16 bytes
+  longlong2* part = static_cast<longlong2*>(scratch);
+  fin::k_partials<<<nblk, fin::T, 0, st>>>(hist, nbins, part);
+  fin::k_scan_partials<<<1, 1024, 0, st>>>(part, nblk, count);
+  fin::k_write<<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi);
   return cudaGetLastError();
 }
 
