@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "bits.cuh"
 #include "ecc_common.cuh"
@@ -45,7 +46,7 @@ constexpr int HWORDS = 32768;           // 65536 packed halves
 constexpr int PWORDS = 2048;            // 65536 occupancy bits
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
-constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + (HWORDS + PWORDS) * 4;
+constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + (HWORDS + PWORDS + 1) * 4;  // + set-bit count
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr uint32_t BIAS = 0x80008000u;  // both halves at 32768
 
@@ -287,47 +288,67 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
       bits::transpose8(V);  // byte b of V[r] = int8 change of voxel 8b + r
       const uint32_t hbase = smem_u32(hwords), pbase = smem_u32(pres);
       // branch-free per voxel: predicated shared-memory ops (no divergence
-      // bookkeeping), the rare out-of-band fix behind a warp vote
+      // bookkeeping), the rare out-of-band fix behind a warp vote.  Once
+      // every bin's occupancy bit is set (random 16-bit data fills the map
+      // early) the occupancy code is skipped for the whole step.
+      auto voxels = [&](auto with_presence) {
 #pragma unroll
-      for (int p = 1; p <= 30; ++p) {
-        const int r = p & 7, b = p >> 3;
-        const uint32_t chu = bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
-        const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
-        // occupancy: set the bit only when this lane owns the voxel and it is not set yet
-        {
-          const uint32_t pa = pbase + ((key >> 3) & ~3u);
-          const uint32_t bit = 1u << (key & 31);
-          uint32_t pw;
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
-          const uint32_t need = ((vm >> p) & 1u) & (uint32_t)((pw & bit) == 0);
+        for (int p = 1; p <= 30; ++p) {
+          const int r = p & 7, b = p >> 3;
+          const uint32_t chu =
+              bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
+          const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
+          if constexpr (decltype(with_presence)::value) {
+            const uint32_t pa = pbase + ((key >> 3) & ~3u);
+            const uint32_t bit = 1u << (key & 31);
+            uint32_t pw;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
+            const uint32_t need = ((vm >> p) & 1u) & (uint32_t)((pw & bit) == 0);
+            uint32_t prev;
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %3;\n\t"
+                "@q atom.shared.or.b32 %0, [%2], %3;\n\t}"
+                : "=r"(prev)
+                : "r"(need), "r"(pa), "r"(bit)
+                : "memory");
+            // count newly set bits so the map's saturation can be detected
+            const uint32_t fresh = need & (uint32_t)((prev & bit) == 0);
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], 1;\n\t}" ::"r"(fresh),
+                "r"(pbase + PWORDS * 4)
+                : "memory");
+          }
+          const uint32_t mult = 1u + 65535u * (key & 1u);  // 1 or 65536: low or high half
+          const uint32_t add = chu * mult;
+          const uint32_t wa = hbase + ((key << 1) & ~3u);
+          uint32_t old;
           asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.or.b32 [%1], %2;\n\t}" ::"r"(need),
-              "r"(pa), "r"(bit)
+              "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
+              "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
+              : "=r"(old)
+              : "r"(chu), "r"(wa), "r"(add), "n"(BIAS)
               : "memory");
-        }
-        const uint32_t sh = (key & 1u) << 4;
-        const uint32_t add = chu << sh;
-        const uint32_t wa = hbase + ((key << 1) & ~3u);
-        uint32_t old;
-        asm volatile(
-            "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
-            "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
-            : "=r"(old)
-            : "r"(chu), "r"(wa), "r"(add), "n"(BIAS)
-            : "memory");
-        // band(x) = bit 15 ^ bit 14 of the half; any band change -> spill
-        // what this thread saw (exact whatever its direction)
-        const uint32_t d = old ^ (old + add);
-        const uint32_t cross = (d ^ (d << 1)) & (0x8000u << sh);
-        if (__any_sync(FULL, cross != 0)) {
-          if (cross) {
-            const int after = (int)(((old + add) >> sh) & 0xFFFFu) - 32768;
-            atomicAdd(&hwords[key >> 1], (uint32_t)(-after) << sh);
-            atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[key]),
-                      static_cast<unsigned long long>(static_cast<long long>(after)));
+          // band(x) = bit 15 ^ bit 14 of the half; a band change -> spill
+          // what this thread saw (exact whatever its direction)
+          const uint32_t d = old ^ (old + add);
+          const uint32_t cross = (d ^ (d << 1)) & (0x8000u * mult);
+          if (__any_sync(FULL, cross != 0)) {
+            if (cross) {
+              const uint32_t sh = (key & 1u) << 4;
+              const int after = (int)(((old + add) >> sh) & 0xFFFFu) - 32768;
+              atomicAdd(&hwords[key >> 1], (uint32_t)(-after) << sh);
+              atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[key]),
+                        static_cast<unsigned long long>(static_cast<long long>(after)));
+            }
           }
         }
-      }
+      };
+      uint32_t nset;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nset) : "r"(pbase + PWORDS * 4) : "memory");
+      if (nset >= g.nbins)
+        voxels(std::false_type{});
+      else
+        voxels(std::true_type{});
     }
     xc.gxa = gxa; xc.gxz = gxz; xc.gxz1 = gxz1; xc.gxy = gxy; xc.gxyu = gxyu;
     xc.g8 = g8; xc.g81 = g81; xc.g8u = g8u; xc.g8u1 = g8u1;
@@ -346,7 +367,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   uint8_t(*myring)[STAGE] = ring[warp];
   uint64_t* myfull = full[warp];
   for (int i = threadIdx.x; i < HWORDS; i += NW * 32) hwords[i] = BIAS;
-  for (int i = threadIdx.x; i < PWORDS; i += NW * 32) pres[i] = 0;
+  for (int i = threadIdx.x; i <= PWORDS; i += NW * 32) pres[i] = 0;  // bitmap + count
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&myfull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

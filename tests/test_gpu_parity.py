@@ -398,3 +398,19 @@ def test_memory_budget_plan_streams_out_of_core_shape(ctx):
     assert v.total() == 1
     q = ctx.vcec(img)
     assert np.array_equal(v.changes, q.changes)
+
+
+@pytest.mark.slow
+def test_u16_spill_path_isolated_minima(ctx):
+    """Adversarial input for the packed 16-bit shared histogram of the u16
+    kernel: 256^3 isolated minima share one value, so that bin's running
+    sum crosses the +-16384 band many times in every CTA and the exact spill
+    path runs; the whole VCEC must still equal the oracle's."""
+    rng = np.random.default_rng(99)
+    img = rng.integers(1000, 60000, (512, 512, 512)).astype(np.uint16)
+    img[::2, ::2, ::2] = 0
+    got = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(got.values.astype(np.int64), v.astype(np.int64))
+    assert np.array_equal(got.changes, c)
+    assert got.changes[0] == 256 ** 3
