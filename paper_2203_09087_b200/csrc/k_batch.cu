@@ -163,6 +163,10 @@ __global__ void __launch_bounds__(NT, 1)
   for (uint32_t q = threadIdx.x; q < nbins / 32; q += NT) pres_row[q] = pres[q];
 }
 
+bool batch16_supported(int h, int w);
+cudaError_t launch_batch16(const uint16_t* data, uint64_t count, int h, int w, int32_t* chi,
+                           uint32_t* presence, int32_t* spill_scratch, cudaStream_t st);
+
 cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, int w,
                            int32_t* chi, uint32_t* presence, int32_t* spill_scratch,
                            cudaStream_t st) {
@@ -172,6 +176,9 @@ cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, i
     const size_t smem = (nbins + nbins / 32) * 4;
     k_batch2d<uint8_t, false><<<(unsigned)count, NT, smem, st>>>(
         (const uint8_t*)data, h, w, nbins, chi, presence, nullptr);
+  } else if (dtype == 1 && batch16_supported(h, w)) {
+    return launch_batch16(static_cast<const uint16_t*>(data), count, h, w, chi, presence,
+                          spill_scratch, st);
   } else if (dtype == 1) {
     const uint32_t nbins = 65536;
     const size_t smem = (nbins / 2 + 2 * nbins / 32) * 4;

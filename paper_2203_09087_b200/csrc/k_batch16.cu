@@ -1,0 +1,298 @@
+// k_batch16.cu -- batched 2D ECC for u16 images (BASELINE config 3), bit
+// sliced.  One CTA per image; the image's 65536-bin histogram lives in
+// shared memory (packed biased 16-bit halves with exact spills, as in
+// k_u16_3d.cu) and the epilogue writes the dense chi row + occupancy bitmap.
+//
+// Mapping.  A lane owns a 32-pixel chunk of a row (bit p = pixel 32c + p
+// along axis 1) and sweeps a band of rows (axis 0); the L lanes of a band
+// hold the row's consecutive chunks, so a pixel's axis-1 neighbour across a
+// chunk boundary arrives by a warp shuffle (funnel shift) -- no halo bits.
+// Per row the lane bit-transposes its 32 keys into 16 planes, then, with the
+// tie rule of change_2d (kernel.hpp:81-94; ties go to the earlier pixel):
+//   pairs along axis 1: gz = [c(p) > c(p+1)], pair minimum mz;
+//   pairs along axis 0: gx = [P(p) > N(p)] between consecutive rows;
+//   2 x 2 quads: gq = [mz of row X-1 > mz of row X];
+// and a pixel of row X-1 changes chi by 1 + #quads won - #pairs won
+// (range [-3, 1]).  The 8 win bits go through a small
+// carry-save adder; the result minus 3 is the change in 4-bit two's
+// complement, transposed back to signed bytes for the histogram.
+#include <cub/cub.cuh>
+#include <type_traits>
+
+#include "bits.cuh"
+#include "ecc_common.cuh"
+#include "internal.h"
+
+namespace eccb {
+namespace b16 {
+
+constexpr int NW = 16;  // warps per CTA
+constexpr int NT = NW * 32;
+constexpr int HWORDS = 32768, PWORDS = 2048;
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr uint32_t BIAS = 0x80008000u;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// 32 keys (two per word, natural order) -> 16 bit planes
+__device__ __forceinline__ void planes16(const uint32_t (&W)[16], uint32_t (&C)[16]) {
+  uint32_t lo[8], hi[8], t[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    lo[j] = bits::prmt(W[2 * j], W[2 * j + 1], 0x6420);
+    hi[j] = bits::prmt(W[2 * j], W[2 * j + 1], 0x7531);
+  }
+  bits::byte_interleave(lo, t);
+  bits::transpose8(t);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) C[i] = t[i];
+  bits::byte_interleave(hi, t);
+  bits::transpose8(t);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) C[8 + i] = t[i];
+}
+
+struct Row {
+  uint32_t C[16], mz[16];
+  uint32_t gz;
+  uint32_t W[16];
+};
+
+__global__ void __launch_bounds__(NT, 1)
+    k_batch16(const uint16_t* __restrict__ data, int h, int w, int L, int32_t* __restrict__ chi,
+              uint32_t* __restrict__ presence, int32_t* __restrict__ spill_scratch) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* hw = sm;                    // packed halves
+  uint32_t* pres = hw + HWORDS;         // occupancy bits
+  uint32_t* spilled = pres + PWORDS;    // bins with a spilled partial in `scratch`
+  for (int i = threadIdx.x; i < HWORDS; i += NT) hw[i] = BIAS;
+  for (int i = threadIdx.x; i < 2 * PWORDS; i += NT) pres[i] = 0;
+  __syncthreads();
+  const uint16_t* img = data + (size_t)blockIdx.x * h * w;
+  int32_t* scratch = spill_scratch + (size_t)smid() * 65536;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunks = (w + 31) / 32;
+  const int bpw = 32 / L;                       // bands per warp
+  const int nbands = NW * bpw;
+  const int band = warp * bpw + lane / L, c = lane % L;
+  // every band runs the same number of row steps (warp-wide shuffles stay
+  // converged); rows past the image are collar and emit nothing
+  const int rows = (h + nbands - 1) / nbands;
+  const int R0 = band * rows;
+  // pixels of this chunk outside [0, w) (all of them for dummy lanes)
+  const int lo = 32 * c;
+  uint32_t zout = FULL;
+  if (c < nchunks) zout = (w - lo >= 32) ? 0u : (FULL << (w - lo));
+  const uint32_t vm = ~zout;
+  const bool first = c == 0, last = c == nchunks - 1;
+  const bool vec = (w & 7) == 0;
+  const uint32_t hbase = smem_u32(hw), pbase = smem_u32(pres);
+
+  auto load_row = [&](int i, uint32_t (&W)[16]) {
+    if (i < 0 || i >= h || c >= nchunks) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) W[j] = FULL;
+      return;
+    }
+    const uint16_t* p = img + (size_t)i * w + lo;
+    if (vec && w - lo >= 32) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + q);
+        W[4 * q] = v.x; W[4 * q + 1] = v.y; W[4 * q + 2] = v.z; W[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint32_t a = (lo + 2 * j < w) ? __ldg(p + 2 * j) : 0xFFFFu;
+        const uint32_t b = (lo + 2 * j + 1 < w) ? __ldg(p + 2 * j + 1) : 0xFFFFu;
+        W[j] = a | (b << 16);
+      }
+    }
+  };
+
+  Row A, B;
+  uint32_t xgx = 0, xgq = 0, xgq1 = 0;  // previous row pair's results
+  uint32_t nxt[16];
+  load_row(R0 - 1, nxt);
+  // steps: rows R0-1 .. R0+rows arrive; at the arrival of row X the changes
+  // of row X-1 are emitted (X-1 in [R0, R0 + rows) and inside the image)
+  auto step = [&](int X, Row& P, Row& N, auto kind) {
+    constexpr int K = decltype(kind)::value;  // 0 first, 1 no emission, 2 emit
+#pragma unroll
+    for (int j = 0; j < 16; ++j) N.W[j] = nxt[j];
+    load_row(X + 1, nxt);  // prefetch (collar past the band's last row + 1 is harmless)
+    planes16(N.W, N.C);
+    const bool xout = X < 0 || X >= h;
+    const uint32_t om = xout ? FULL : zout;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) N.C[i] |= om;
+    {
+      uint32_t t[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint32_t nb = __shfl_down_sync(FULL, N.C[i], 1, L);
+        if (last) nb = FULL;  // right collar (later side: loses every tie)
+        t[i] = __funnelshift_r(N.C[i], nb, 1);
+      }
+      N.gz = bits::gt<16>(N.C, t);
+      bits::sel<16>(N.mz, N.gz, N.C, t);
+    }
+    if constexpr (K >= 1) {
+      uint32_t gx = bits::gt<16>(P.C, N.C);
+      uint32_t gq = bits::gt<16>(P.mz, N.mz);
+      if (X - 1 < 0) gx = gq = FULL;  // row -1 never wins
+      // quad anchored one pixel to the left: from the previous chunk, or for
+      // the first chunk the quad over the left collar, whose minima are the
+      // pixels at 0 -- its comparison is gx bit 0
+      uint32_t qprev = __shfl_up_sync(FULL, gq, 1, L);
+      if (first) qprev = gx << 31;
+      const uint32_t gq1 = __funnelshift_l(qprev, gq, 1);
+      if constexpr (K == 2) {
+        uint32_t zprev = __shfl_up_sync(FULL, P.gz, 1, L);
+        if (first) zprev = FULL;  // the left collar never wins
+        const uint32_t Z0 = ~P.gz;
+        const uint32_t Z1 = __funnelshift_l(zprev, P.gz, 1);
+        // S = 4 quads won + 4 negated pairs won = change + 3
+        const uint32_t t0 = Z0 & ~gq, t1 = Z0 & xgq, t2 = Z1 & ~gq1, t3 = Z1 & xgq1;
+        const uint32_t t4 = ~Z0, t5 = ~Z1, t6 = gx, t7 = ~xgx;
+        uint32_t s0, c0, s1, c1, s2, c2;
+        bits::fa3(t0, t1, t2, s0, c0);
+        bits::fa3(t3, t4, t5, s1, c1);
+        bits::fa3(t6, t7, s0, s2, c2);
+        const uint32_t b0 = s1 ^ s2, k0 = s1 & s2;             // weight 1
+        uint32_t b1, k1;
+        bits::fa3(c0, c1, c2, b1, k1);                         // weight 2
+        const uint32_t b1x = b1 ^ k0, k1x = b1 & k0;
+        const uint32_t b2 = k1 ^ k1x;                          // weight 4 (S <= 4)
+        // d = S - 3 (mod 16), 4-bit two's complement, masked to owned pixels
+        // S - 3 = S + 13: add 1101b
+        const uint32_t d0 = ~b0;                               // b0 + 1
+        const uint32_t cy1 = b0;
+        const uint32_t d1 = b1x ^ cy1;                         // + 0
+        const uint32_t cy2 = b1x & cy1;
+        const uint32_t d2 = ~(b2 ^ cy2);                       // + 1
+        const uint32_t cy3 = b2 | cy2;
+        const uint32_t d3 = ~cy3;                              // + 1 (no carry out needed)
+        const uint32_t vmr = (X - 1 < h) ? vm : 0u;
+        uint32_t V[8] = {d0 & vmr, d1 & vmr, d2 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr};
+        bits::transpose8(V);
+        auto pixels = [&](auto with_presence) {
+#pragma unroll
+          for (int p = 0; p < 32; ++p) {
+            const int r = p & 7, b = p >> 3;
+            const uint32_t chu =
+                bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
+            const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
+            if constexpr (decltype(with_presence)::value) {
+              const uint32_t pa = pbase + ((key >> 3) & ~3u);
+              const uint32_t bit = 1u << (key & 31);
+              uint32_t pw;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
+              const uint32_t need = ((vmr >> p) & 1u) & (uint32_t)((pw & bit) == 0);
+              asm volatile(
+                  "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.or.b32 [%1], %2;\n\t}" ::"r"(need),
+                  "r"(pa), "r"(bit)
+                  : "memory");
+            }
+            const uint32_t mult = 1u + 65535u * (key & 1u);
+            const uint32_t add = chu * mult;
+            const uint32_t wa = hbase + ((key << 1) & ~3u);
+            uint32_t old;
+            asm volatile(
+                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
+                "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
+                : "=r"(old)
+                : "r"(chu), "r"(wa), "r"(add), "n"(BIAS)
+                : "memory");
+            const uint32_t dd = old ^ (old + add);
+            const uint32_t cross = (dd ^ (dd << 1)) & (0x8000u * mult);
+            if (__any_sync(FULL, cross != 0)) {
+              if (cross) {
+                const uint32_t sh = (key & 1u) << 4;
+                const int after = (int)(((old + add) >> sh) & 0xFFFFu) - 32768;
+                atomicAdd(&hw[key >> 1], (uint32_t)(-after) << sh);
+                atomicAdd(&scratch[key], after);
+                atomicOr(&spilled[key >> 5], 1u << (key & 31));
+              }
+            }
+          }
+        };
+        // skip the occupancy code for rows whose keys are all marked already
+        // is not decidable cheaply; it always runs (u16 images rarely fill
+        // all 65536 bins)
+        pixels(std::true_type{});
+      }
+      xgx = gx;
+      xgq = gq;
+      xgq1 = gq1;
+    }
+  };
+  step(R0 - 1, B, A, std::integral_constant<int, 0>{});
+  step(R0, A, B, std::integral_constant<int, 1>{});
+  int X = R0 + 1;
+  for (; X + 1 <= R0 + rows; X += 2) {
+    step(X, B, A, std::integral_constant<int, 2>{});
+    step(X + 1, A, B, std::integral_constant<int, 2>{});
+  }
+  if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
+  __syncthreads();
+  // epilogue: thread t owns bins [t * 128, (t + 1) * 128)
+  constexpr uint32_t per = 65536 / NT;
+  const uint32_t b0 = threadIdx.x * per;
+  int32_t* row = chi + (size_t)blockIdx.x * 65536;
+  auto bin_sum = [&](uint32_t b) -> int {
+    int s = (int)((hw[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
+    if ((spilled[b >> 5] >> (b & 31)) & 1u) s += scratch[b];
+    return s;
+  };
+  int32_t local = 0;
+  for (uint32_t b = b0; b < b0 + per; ++b) local += bin_sum(b);
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  int32_t ex;
+  Scan(tmp).ExclusiveSum(local, ex);
+  for (uint32_t b = b0; b < b0 + per; b += 4) {
+    int4 o;
+    ex += bin_sum(b); o.x = ex;
+    ex += bin_sum(b + 1); o.y = ex;
+    ex += bin_sum(b + 2); o.z = ex;
+    ex += bin_sum(b + 3); o.w = ex;
+    *reinterpret_cast<int4*>(row + b) = o;
+  }
+  __syncthreads();  // every read of the scratch row is done
+  for (uint32_t b = b0; b < b0 + per; ++b)
+    if ((spilled[b >> 5] >> (b & 31)) & 1u) scratch[b] = 0;
+  uint32_t* pres_row = presence + (size_t)blockIdx.x * PWORDS;
+  for (int q = threadIdx.x; q < PWORDS; q += NT) pres_row[q] = pres[q];
+}
+
+}  // namespace b16
+
+bool batch16_supported(int h, int w) { return w >= 1 && w <= 1024 && h >= 1; }
+
+cudaError_t launch_batch16(const uint16_t* data, uint64_t count, int h, int w, int32_t* chi,
+                           uint32_t* presence, int32_t* spill_scratch, cudaStream_t st) {
+  using namespace b16;
+  if (count == 0) return cudaSuccess;
+  int L = 1;
+  while (L < (w + 31) / 32) L <<= 1;
+  const size_t smem = (size_t)(HWORDS + 2 * PWORDS) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_batch16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_batch16<<<(unsigned)count, NT, smem, st>>>(data, h, w, L, chi, presence, spill_scratch);
+  return cudaGetLastError();
+}
+
+}  // namespace eccb
