@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "bits.cuh"
+#include "hist16.cuh"
 #include "ecc_common.cuh"
 #include "internal.h"
 
@@ -185,51 +186,32 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t vmr = (X - 1 < h) ? vm : 0u;
         uint32_t V[8] = {d0 & vmr, d1 & vmr, d2 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr};
         bits::transpose8(V);
-        auto pixels = [&](auto with_presence) {
+        // histogram: groups of 4 pixels (atomic latencies overlap), one vote
+        // per group for the rare out-of-band fix
+        auto spill = [&](uint32_t key, int after) {
+          atomicAdd(&scratch[key], after);
+          atomicOr(&spilled[key >> 5], 1u << (key & 31));
+        };
 #pragma unroll
-          for (int p = 0; p < 32; ++p) {
-            const int r = p & 7, b = p >> 3;
+        for (int g4 = 0; g4 < 32; g4 += 4) {
+          hist16::Upd u[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int p = g4 + j, r = p & 7, b = p >> 3;
             const uint32_t chu =
                 bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
             const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
-            if constexpr (decltype(with_presence)::value) {
-              const uint32_t pa = pbase + ((key >> 3) & ~3u);
-              const uint32_t bit = 1u << (key & 31);
-              uint32_t pw;
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
-              const uint32_t need = ((vmr >> p) & 1u) & (uint32_t)((pw & bit) == 0);
-              asm volatile(
-                  "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.or.b32 [%1], %2;\n\t}" ::"r"(need),
-                  "r"(pa), "r"(bit)
-                  : "memory");
-            }
-            const uint32_t mult = 1u + 65535u * (key & 1u);
-            const uint32_t add = chu * mult;
-            const uint32_t wa = hbase + ((key << 1) & ~3u);
-            uint32_t old;
-            asm volatile(
-                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
-                "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
-                : "=r"(old)
-                : "r"(chu), "r"(wa), "r"(add), "n"(BIAS)
-                : "memory");
-            const uint32_t dd = old ^ (old + add);
-            const uint32_t cross = (dd ^ (dd << 1)) & (0x8000u * mult);
-            if (__any_sync(FULL, cross != 0)) {
-              if (cross) {
-                const uint32_t sh = (key & 1u) << 4;
-                const int after = (int)(((old + add) >> sh) & 0xFFFFu) - 32768;
-                atomicAdd(&hw[key >> 1], (uint32_t)(-after) << sh);
-                atomicAdd(&scratch[key], after);
-                atomicOr(&spilled[key >> 5], 1u << (key & 31));
-              }
-            }
+            hist16::mark(pbase, key, (vmr >> p) & 1u);
+            hist16::issue(hbase, key, chu, u[j]);
           }
-        };
-        // skip the occupancy code for rows whose keys are all marked already
-        // is not decidable cheaply; it always runs (u16 images rarely fill
-        // all 65536 bins)
-        pixels(std::true_type{});
+          uint32_t cr[4], any = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          if (__any_sync(FULL, any != 0)) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) hist16::fix(hbase, u[j], cr[j], spill);
+          }
+        }
       }
       xgx = gx;
       xgq = gq;

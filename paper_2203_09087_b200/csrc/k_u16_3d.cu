@@ -31,6 +31,7 @@
 #include <type_traits>
 
 #include "bits.cuh"
+#include "hist16.cuh"
 #include "ecc_common.cuh"
 #include "internal.h"
 
@@ -291,55 +292,50 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
       // bookkeeping), the rare out-of-band fix behind a warp vote.  Once
       // every bin's occupancy bit is set (random 16-bit data fills the map
       // early) the occupancy code is skipped for the whole step.
+      auto spill = [&](uint32_t key, int after) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[key]),
+                  static_cast<unsigned long long>(static_cast<long long>(after)));
+      };
       auto voxels = [&](auto with_presence) {
+        // groups of voxels: atomic latencies overlap, one vote per group for
+        // the rare out-of-band fix (hist16.cuh)
 #pragma unroll
-        for (int p = 1; p <= 30; ++p) {
-          const int r = p & 7, b = p >> 3;
-          const uint32_t chu =
-              bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
-          const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
-          if constexpr (decltype(with_presence)::value) {
-            const uint32_t pa = pbase + ((key >> 3) & ~3u);
-            const uint32_t bit = 1u << (key & 31);
-            uint32_t pw;
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
-            const uint32_t need = ((vm >> p) & 1u) & (uint32_t)((pw & bit) == 0);
-            uint32_t prev;
-            asm volatile(
-                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %3;\n\t"
-                "@q atom.shared.or.b32 %0, [%2], %3;\n\t}"
-                : "=r"(prev)
-                : "r"(need), "r"(pa), "r"(bit)
-                : "memory");
-            // count newly set bits so the map's saturation can be detected
-            const uint32_t fresh = need & (uint32_t)((prev & bit) == 0);
-            asm volatile(
-                "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], 1;\n\t}" ::"r"(fresh),
-                "r"(pbase + PWORDS * 4)
-                : "memory");
-          }
-          const uint32_t mult = 1u + 65535u * (key & 1u);  // 1 or 65536: low or high half
-          const uint32_t add = chu * mult;
-          const uint32_t wa = hbase + ((key << 1) & ~3u);
-          uint32_t old;
-          asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
-              "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
-              : "=r"(old)
-              : "r"(chu), "r"(wa), "r"(add), "n"(BIAS)
-              : "memory");
-          // band(x) = bit 15 ^ bit 14 of the half; a band change -> spill
-          // what this thread saw (exact whatever its direction)
-          const uint32_t d = old ^ (old + add);
-          const uint32_t cross = (d ^ (d << 1)) & (0x8000u * mult);
-          if (__any_sync(FULL, cross != 0)) {
-            if (cross) {
-              const uint32_t sh = (key & 1u) << 4;
-              const int after = (int)(((old + add) >> sh) & 0xFFFFu) - 32768;
-              atomicAdd(&hwords[key >> 1], (uint32_t)(-after) << sh);
-              atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[key]),
-                        static_cast<unsigned long long>(static_cast<long long>(after)));
+        for (int g5 = 1; g5 <= 30; g5 += 5) {
+          hist16::Upd u[5];
+#pragma unroll
+          for (int j = 0; j < 5; ++j) {
+            const int p = g5 + j, r = p & 7, b = p >> 3;
+            const uint32_t chu =
+                bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
+            const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
+            if constexpr (decltype(with_presence)::value) {
+              const uint32_t pa = pbase + ((key >> 3) & ~3u);
+              const uint32_t bit = 1u << (key & 31);
+              uint32_t pw;
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
+              const uint32_t need = ((vm >> p) & 1u) & (uint32_t)((pw & bit) == 0);
+              uint32_t prev;
+              asm volatile(
+                  "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %3;\n\t"
+                  "@q atom.shared.or.b32 %0, [%2], %3;\n\t}"
+                  : "=r"(prev)
+                  : "r"(need), "r"(pa), "r"(bit)
+                  : "memory");
+              // count newly set bits so the map's saturation can be detected
+              const uint32_t fresh = need & (uint32_t)((prev & bit) == 0);
+              asm volatile(
+                  "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.add.u32 [%1], 1;\n\t}" ::"r"(fresh),
+                  "r"(pbase + PWORDS * 4)
+                  : "memory");
             }
+            hist16::issue(hbase, key, chu, u[j]);
+          }
+          uint32_t cr[5], any = 0;
+#pragma unroll
+          for (int j = 0; j < 5; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          if (__any_sync(FULL, any != 0)) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j) hist16::fix(hbase, u[j], cr[j], spill);
           }
         }
       };
