@@ -647,6 +647,13 @@ def process_image(image, plan: ChunkPlan = None, options: EngineOptions = None,
             plan = _even_plan(image.dims().w0, 1)
         return ctx.process_source(image, plan, options, report, binmap)
     if plan is not None and not _is_torch_cuda(image):
+        arr = image if isinstance(image, np.ndarray) else np.asarray(image)
+        sorted_f32 = arr.dtype == np.float32 and (binmap is None or
+                                                  _binmap(ECC_F32, binmap).kind == ECC_BIN_SORTED)
+        if not sorted_f32 and options.ingest_delay_ms <= 0:
+            # the whole image is already in host memory: chunks are DMA-copied
+            # straight from it (ecc_process_host), no read_rows round trip
+            return ctx.process_host(arr, plan, report, binmap)
         return ctx.process_source(MemorySource(image), plan, options, report, binmap)
     return ctx.vcec(image, binmap)
 

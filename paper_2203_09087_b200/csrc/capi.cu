@@ -219,6 +219,20 @@ int check_slab(ecc_dims d, uint64_t plane0, uint64_t nplanes, uint64_t own0,
   return ECC_OK;
 }
 
+// Plan validation with the reference's messages (streaming.hpp:186-195):
+// bounds[0..nchunks] must be 0 = b0 < b1 < ... < b_n = w0.
+int check_plan(const uint64_t* bounds, size_t nchunks, const ecc_dims& dims) {
+  if (nchunks == 0 || !bounds) return fail(ECC_EINVAL, "empty chunk plan");
+  if (bounds[0] != 0) return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  for (size_t k = 0; k < nchunks; ++k)
+    if (bounds[k + 1] <= bounds[k])
+      return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
+  if (bounds[nchunks] != dims.w0)
+    return fail(ECC_EINVAL, "chunk plan covers [0, " + std::to_string(bounds[nchunks]) +
+                                ") but the source has w0 = " + std::to_string(dims.w0));
+  return ECC_OK;
+}
+
 Slab make_slab(const void* base, ecc_dims d, uint64_t plane0, uint64_t nplanes,
                uint64_t own0, uint64_t own1) {
   Slab s;
@@ -750,15 +764,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   CKI(check_dims(dims));
   if (!read_rows || !values_out || !changes_out || !n_out)
     return fail(ECC_EINVAL, "null pointer");
-  // plan validation, streaming.hpp:186-195
-  if (nchunks == 0 || !bounds) return fail(ECC_EINVAL, "empty chunk plan");
-  if (bounds[0] != 0) return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
-  for (size_t k = 0; k < nchunks; ++k)
-    if (bounds[k + 1] <= bounds[k])
-      return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
-  if (bounds[nchunks] != dims.w0)
-    return fail(ECC_EINVAL, "chunk plan covers [0, " + std::to_string(bounds[nchunks]) +
-                                ") but the source has w0 = " + std::to_string(dims.w0));
+  CKI(check_plan(bounds, nchunks, dims));
   uint64_t nbins = 0;
   bool affine = false, sorted = false;
   AffineMap am{};
@@ -990,14 +996,7 @@ int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims d
   CKI(check_dtype(dtype));
   CKI(check_dims(dims));
   if (!host || !values_out || !changes_out || !n_out) return fail(ECC_EINVAL, "null pointer");
-  if (nchunks == 0 || !bounds) return fail(ECC_EINVAL, "empty chunk plan");
-  if (bounds[0] != 0) return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
-  for (size_t k = 0; k < nchunks; ++k)
-    if (bounds[k + 1] <= bounds[k])
-      return fail(ECC_EINVAL, "chunk plan does not cover the image contiguously");
-  if (bounds[nchunks] != dims.w0)
-    return fail(ECC_EINVAL, "chunk plan covers [0, " + std::to_string(bounds[nchunks]) +
-                                ") but the source has w0 = " + std::to_string(dims.w0));
+  CKI(check_plan(bounds, nchunks, dims));
   uint64_t nbins = 0;
   bool affine = false, sorted = false;
   AffineMap am{};
