@@ -141,6 +141,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the N > 1 path on a box with fewer GPUs "
+                         "(ranks then share devices; the timing is not a scaling number)")
     args = ap.parse_args()
     warmup = max(3, args.warmup)
 
@@ -169,11 +172,15 @@ def main():
     import torch
     import paper_2203_09087_b200 as eb
 
+    local = local % max(1, torch.cuda.device_count())  # gloo test runs may share a GPU
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     ctx = eb.Context(local)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -319,7 +326,7 @@ def main():
            "data": "synthetic (counter_hash seed 1, SURVEY.md 8(d)); device-generated",
            "config": {"workload": "C2: 512^3 u8 3D ECC per GPU (z-slab of a (512N)x512x512 volume)",
                       "voxels_per_gpu": SIDE ** 3, "bins": 256,
-                      "parallelism": f"zslab{n}" + ("+nccl_allreduce" if n > 1 else ""),
+                      "parallelism": f"zslab{n}" + (f"+{args.dist_backend}_allreduce" if n > 1 else ""),
                       "l2": "flushed between timed steps (256 MiB write)"},
            "kernel_ms": t_kern,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
