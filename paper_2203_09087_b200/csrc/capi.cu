@@ -137,6 +137,8 @@ struct ecc_ctx {
   DevBuf fused;  // ticket + 512 x int64 histogram of the fused u8 launch (kept zero)
   DevBuf pad;       // row-padded copy of a u8 slab for the TMA kernel
   DevBuf finscr;    // K3 partials for large bin counts
+  DevBuf res;       // result block (count, flags, curve) read back in one copy
+  PinBuf res_host;
   DevBuf keys16;    // 16-bit keys (u16 padded / f32 bin indices) for k_u16_3d
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
@@ -359,45 +361,63 @@ int launch_fused(ecc_ctx* ctx, const Slab& s, uint32_t* bins, int64_t* changes, 
   return ECC_OK;
 }
 
-int copy_result_to_host(ecc_ctx* ctx, cudaStream_t st, BinResult* out) {
-  uint64_t m = 0;
-  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
-  CKR(cudaStreamSynchronize(st));
-  out->bins.resize(m);
-  out->changes.resize(m);
-  out->chi.resize(m);
-  if (m) {
-    CKR(cudaMemcpyAsync(out->bins.data(), ctx->bins.p, m * 4, cudaMemcpyDeviceToHost, st));
-    CKR(cudaMemcpyAsync(out->changes.data(), ctx->changes.p, m * 8, cudaMemcpyDeviceToHost, st));
-    CKR(cudaMemcpyAsync(out->chi.data(), ctx->chi.p, m * 8, cudaMemcpyDeviceToHost, st));
-    CKR(cudaStreamSynchronize(st));
+// One device block holds everything a host caller reads back -- the
+// occurring-bin count, the error flags and the compacted curve -- so a call
+// ends with ONE device-to-host copy and one synchronisation:
+//   [0, 8) count | [8, 12) flags | [64, ...) bins u32 | changes i64 | chi i64
+struct ResultLayout {
+  size_t bins, changes, chi, bytes;
+  explicit ResultLayout(uint64_t nbins) {
+    bins = 64;
+    changes = bins + ((nbins * 4 + 7) & ~7ull);
+    chi = changes + nbins * 8;
+    bytes = chi + nbins * 8;
   }
+};
+
+int result_block(ecc_ctx* ctx, uint64_t nbins, ResultLayout* L) {
+  *L = ResultLayout(nbins);
+  CKI(ctx->res.ensure(L->bytes));
+  CKI(ctx->res_host.ensure(L->bytes));
   return ECC_OK;
 }
 
-int finalize_to_host(ecc_ctx* ctx, uint32_t nbins, cudaStream_t st, BinResult* out) {
-  CKI(ctx->bins.ensure(nbins * 4ull));
-  CKI(ctx->changes.ensure(nbins * 8ull));
-  CKI(ctx->chi.ensure(nbins * 8ull));
-  CKI(ctx->count.ensure(8));
-  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
-  CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, ctx->bins.as<uint32_t>(),
-                      ctx->changes.as<int64_t>(), ctx->chi.as<int64_t>(),
-                      ctx->count.as<uint64_t>(), ctx->finscr.p, st));
-  ctx->launches += 1;
-  uint64_t m = 0;
-  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+// The flags are copied into the block, the block comes back in one copy,
+// and flag errors are reported with the wording of read_flags().
+int fetch_result(ecc_ctx* ctx, const ResultLayout& L, cudaStream_t st, BinResult* out) {
+  uint8_t* d = ctx->res.as<uint8_t>();
+  uint8_t* h = static_cast<uint8_t*>(ctx->res_host.p);
+  if (ctx->flags.p) CKR(cudaMemcpyAsync(d + 8, ctx->flags.p, 4, cudaMemcpyDeviceToDevice, st));
+  else CKR(cudaMemsetAsync(d + 8, 0, 4, st));
+  CKR(cudaMemcpyAsync(h, d, L.bytes, cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
-  out->bins.resize(m);
-  out->changes.resize(m);
-  out->chi.resize(m);
-  if (m) {
-    CKR(cudaMemcpyAsync(out->bins.data(), ctx->bins.p, m * 4, cudaMemcpyDeviceToHost, st));
-    CKR(cudaMemcpyAsync(out->changes.data(), ctx->changes.p, m * 8, cudaMemcpyDeviceToHost, st));
-    CKR(cudaMemcpyAsync(out->chi.data(), ctx->chi.p, m * 8, cudaMemcpyDeviceToHost, st));
-    CKR(cudaStreamSynchronize(st));
-  }
+  uint64_t m;
+  uint32_t f;
+  std::memcpy(&m, h, 8);
+  std::memcpy(&f, h + 8, 4);
+  if (f & kFlagNaN) return fail(ECC_ENAN, "cannot build a value index: NaN input");
+  if (f & kFlagBinmap) return fail(ECC_EBINMAP, "a value does not lie on the affine bin grid");
+  out->bins.assign(reinterpret_cast<const uint32_t*>(h + L.bins),
+                   reinterpret_cast<const uint32_t*>(h + L.bins) + m);
+  out->changes.assign(reinterpret_cast<const int64_t*>(h + L.changes),
+                      reinterpret_cast<const int64_t*>(h + L.changes) + m);
+  out->chi.assign(reinterpret_cast<const int64_t*>(h + L.chi),
+                  reinterpret_cast<const int64_t*>(h + L.chi) + m);
   return ECC_OK;
+}
+
+// K3 over ctx->hist into the result block, then fetch_result.
+int finalize_to_host(ecc_ctx* ctx, uint32_t nbins, cudaStream_t st, BinResult* out) {
+  ResultLayout L(nbins);
+  CKI(result_block(ctx, nbins, &L));
+  uint8_t* d = ctx->res.as<uint8_t>();
+  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
+  CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, reinterpret_cast<uint32_t*>(d + L.bins),
+                      reinterpret_cast<int64_t*>(d + L.changes),
+                      reinterpret_cast<int64_t*>(d + L.chi), reinterpret_cast<uint64_t*>(d),
+                      ctx->finscr.p, st));
+  ctx->launches += 1;
+  return fetch_result(ctx, L, st, out);
 }
 
 // General f32 path (build_index_counts, value_index.hpp:159-197, on the
@@ -525,20 +545,18 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
   Slab sp;
   CKI(pad_for_u8_fast(ctx, s, dtype, affine, st, &sp));
   if (fusable(dtype, sp, affine)) {
-    const Slab& s = sp;
-    CKI(ctx->bins.ensure(nbins * 4ull));
-    CKI(ctx->changes.ensure(nbins * 8ull));
-    CKI(ctx->chi.ensure(nbins * 8ull));
-    CKI(ctx->count.ensure(8));
-    CKI(launch_fused(ctx, s, ctx->bins.as<uint32_t>(), ctx->changes.as<int64_t>(),
-                     ctx->chi.as<int64_t>(), ctx->count.as<uint64_t>(), st));
-    return copy_result_to_host(ctx, st, res);
+    ResultLayout L(nbins);
+    CKI(result_block(ctx, nbins, &L));
+    uint8_t* d = ctx->res.as<uint8_t>();
+    CKI(launch_fused(ctx, sp, reinterpret_cast<uint32_t*>(d + L.bins),
+                     reinterpret_cast<int64_t*>(d + L.changes), reinterpret_cast<int64_t*>(d + L.chi),
+                     reinterpret_cast<uint64_t*>(d), st));
+    return fetch_result(ctx, L, st, res);
   }
   CKI(ctx->hist.ensure(2 * nbins * 8));
   CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
   CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
   CKI(finalize_to_host(ctx, (uint32_t)nbins, st, res));
-  CKI(read_flags(ctx, st));
   return ECC_OK;
 }
 
@@ -606,11 +624,12 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
                     &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad,
-                    &ctx->keys16, &ctx->finscr})
+                    &ctx->keys16, &ctx->finscr, &ctx->res})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
   ctx->host_small.release();
+  ctx->res_host.release();
   cudaStreamDestroy(ctx->stream);
   cudaStreamDestroy(ctx->copy);
   delete ctx;
@@ -902,7 +921,6 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     merge_runs(skeys, ssums, starts, &r);
   } else {
     CKI(finalize_to_host(ctx, (uint32_t)nbins, st, &r));
-    CKI(read_flags(ctx, st));
   }
   // merge phase = the device-side reduction; report it after the kernel
   for (auto& t : tim) {
@@ -1050,7 +1068,6 @@ int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims d
   BinResult r;
   if (rc == ECC_OK) {
     rc = finalize_to_host(ctx, (uint32_t)nbins, st, &r);
-    if (rc == ECC_OK) rc = read_flags(ctx, st);
   }
   CKR(cudaStreamSynchronize(cp));
   CKR(cudaStreamSynchronize(st));
