@@ -139,7 +139,8 @@ struct ecc_ctx {
   DevBuf finscr;    // K3 partials for large bin counts
   DevBuf res;       // result block (count, flags, curve) read back in one copy
   PinBuf res_host;
-  DevBuf keys16;    // 16-bit keys (u16 padded / f32 bin indices) for k_u16_3d
+  DevBuf keys16;
+  DevBuf akeys, asums, sums2;  // sorted f32 path: per-slab runs and their merge    // 16-bit keys (u16 padded / f32 bin indices) for k_u16_3d
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
@@ -428,8 +429,10 @@ struct ToI64 {
   __host__ __device__ int64_t operator()(int8_t v) const { return v; }
 };
 
-int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st,
-                std::vector<uint32_t>* keys_out, std::vector<int64_t>* sums_out) {
+// Appends the slab's reduced (order key, change sum) runs to the device
+// accumulator ctx->akeys / ctx->asums at offset *n (no host round trip).
+int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_voxels,
+                uint64_t* n_acc) {
   const uint64_t n64 = (uint64_t)(s.own1 - s.own0) * s.w1 * s.w2;
   if (n64 > 0x7FFFFFFFull)
     return fail(ECC_EINVAL, "chunk exceeds 2^31 voxels; use a finer chunk plan");
@@ -438,64 +441,93 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st,
   CKI(ctx->keys2.ensure(n64 * 4));
   CKI(ctx->ch8.ensure(n64));
   CKI(ctx->ch8b.ensure(n64));
-  CKI(ctx->sums.ensure(n64 * 8));
   CKI(ctx->count.ensure(8));
+  CKI(ctx->akeys.ensure(total_voxels * 4));
+  CKI(ctx->asums.ensure(total_voxels * 8));
   CKR(launch_generic_changes(s, ECC_F32, ctx->ch8.as<int8_t>(), ctx->sms, st));
   const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
   CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), ctx->flags.as<uint32_t>(),
                         ctx->sms, st));
   ctx->launches += 2;
+  uint32_t* out_keys = ctx->akeys.as<uint32_t>() + *n_acc;
+  int64_t* out_sums = ctx->asums.as<int64_t>() + *n_acc;
   size_t t1 = 0, t2 = 0;
   CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, ctx->keys.as<uint32_t>(),
                                       ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
                                       ctx->ch8b.as<int8_t>(), n, 0, 32, st));
   auto vals = thrust::make_transform_iterator(ctx->ch8b.as<const int8_t>(), ToI64());
-  CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(),
-                                     ctx->keys.as<uint32_t>(), vals, ctx->sums.as<int64_t>(),
-                                     ctx->count.as<uint64_t>(), cub::Sum(), n, st));
+  CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(), out_keys, vals,
+                                     out_sums, ctx->count.as<uint64_t>(), cub::Sum(), n, st));
   CKI(ctx->tmp.ensure(std::max(t1, t2)));
   t1 = ctx->tmp.cap;
   CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, ctx->keys.as<uint32_t>(),
                                       ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
                                       ctx->ch8b.as<int8_t>(), n, 0, 32, st));
   t2 = ctx->tmp.cap;
-  CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(),
-                                     ctx->keys.as<uint32_t>(), vals, ctx->sums.as<int64_t>(),
-                                     ctx->count.as<uint64_t>(), cub::Sum(), n, st));
+  CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(), out_keys, vals,
+                                     out_sums, ctx->count.as<uint64_t>(), cub::Sum(), n, st));
   ctx->launches += 2;
   uint64_t m = 0;
   CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
-  const size_t off = keys_out->size();
-  keys_out->resize(off + m);
-  sums_out->resize(off + m);
-  CKR(cudaMemcpyAsync(keys_out->data() + off, ctx->keys.p, m * 4, cudaMemcpyDeviceToHost, st));
-  CKR(cudaMemcpyAsync(sums_out->data() + off, ctx->sums.p, m * 8, cudaMemcpyDeviceToHost, st));
-  CKR(cudaStreamSynchronize(st));
+  *n_acc += m;
   return ECC_OK;
 }
 
-// merge_local (vcec.hpp:35-66) of sorted (key, sum) runs from several slabs.
-void merge_runs(const std::vector<uint32_t>& keys, const std::vector<int64_t>& sums,
-                const std::vector<size_t>& starts, BinResult* out) {
-  std::vector<std::pair<uint32_t, int64_t>> all;
-  all.reserve(keys.size());
-  for (size_t i = 0; i < keys.size(); ++i) all.emplace_back(keys[i], sums[i]);
-  if (starts.size() > 2) std::stable_sort(all.begin(), all.end(),
-                                          [](auto& a, auto& b) { return a.first < b.first; });
-  out->keys.clear();
-  out->changes.clear();
-  for (auto& [k, v] : all) {
-    if (!out->keys.empty() && out->keys.back() == k)
-      out->changes.back() += v;
-    else {
-      out->keys.push_back(k);
-      out->changes.push_back(v);
-    }
+// merge_local (vcec.hpp:35-66) of every slab's runs on the device: one more
+// sort + reduce-by-key when there were several slabs, then the int64 prefix
+// sum (vcec_to_ecc) and one copy back.
+int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResult* out) {
+  uint32_t* keys = ctx->akeys.as<uint32_t>();
+  int64_t* sums = ctx->asums.as<int64_t>();
+  uint64_t m = n;
+  if (merge && n > 0) {
+    if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "too many distinct values to merge");
+    CKI(ctx->keys.ensure(n * 4));
+    CKI(ctx->keys2.ensure(n * 4));
+    CKI(ctx->sums.ensure(n * 8));
+    CKI(ctx->sums2.ensure(n * 8));
+    size_t t1 = 0, t2 = 0;
+    CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, ctx->keys2.as<uint32_t>(), sums,
+                                        ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
+    CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(),
+                                       ctx->keys.as<uint32_t>(), ctx->sums2.as<int64_t>(),
+                                       ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(),
+                                       cub::Sum(), (int)n, st));
+    CKI(ctx->tmp.ensure(std::max(t1, t2)));
+    t1 = ctx->tmp.cap;
+    CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, keys, ctx->keys2.as<uint32_t>(), sums,
+                                        ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
+    t2 = ctx->tmp.cap;
+    CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(),
+                                       ctx->keys.as<uint32_t>(), ctx->sums2.as<int64_t>(),
+                                       ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(),
+                                       cub::Sum(), (int)n, st));
+    ctx->launches += 2;
+    CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+    keys = ctx->keys.as<uint32_t>();
+    sums = ctx->sums.as<int64_t>();
   }
-  out->chi.resize(out->changes.size());
-  int64_t acc = 0;
-  for (size_t i = 0; i < out->changes.size(); ++i) out->chi[i] = acc += out->changes[i];
+  CKI(ctx->chi.ensure(std::max<uint64_t>(m, 1) * 8));
+  if (m > 0) {
+    size_t t3 = 0;
+    CKR(cub::DeviceScan::InclusiveSum(nullptr, t3, sums, ctx->chi.as<int64_t>(), (int)m, st));
+    CKI(ctx->tmp.ensure(t3));
+    t3 = ctx->tmp.cap;
+    CKR(cub::DeviceScan::InclusiveSum(ctx->tmp.p, t3, sums, ctx->chi.as<int64_t>(), (int)m, st));
+    ctx->launches += 1;
+  }
+  out->keys.resize(m);
+  out->changes.resize(m);
+  out->chi.resize(m);
+  if (m) {
+    CKR(cudaMemcpyAsync(out->keys.data(), keys, m * 4, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->changes.data(), sums, m * 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(out->chi.data(), ctx->chi.p, m * 8, cudaMemcpyDeviceToHost, st));
+  }
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
 }
 
 float key_to_float(uint32_t k) {
@@ -535,12 +567,10 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
   CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
   const Slab s = make_slab(d_data, dims, 0, dims.w0, 0, dims.w0);
   if (sorted) {
-    std::vector<uint32_t> keys;
-    std::vector<int64_t> sums;
-    CKI(sorted_slab(ctx, s, st, &keys, &sums));
+    uint64_t n = 0;
+    CKI(sorted_slab(ctx, s, st, dims.w0 * dims.w1 * dims.w2, &n));
     CKI(read_flags(ctx, st));
-    merge_runs(keys, sums, {0, keys.size()}, res);
-    return ECC_OK;
+    return sorted_finish(ctx, st, n, false, res);
   }
   Slab sp;
   CKI(pad_for_u8_fast(ctx, s, dtype, affine, st, &sp));
@@ -624,7 +654,8 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
                     &ctx->count, &ctx->flags, &ctx->keys, &ctx->keys2, &ctx->ch8,
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
                     &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad,
-                    &ctx->keys16, &ctx->finscr, &ctx->res})
+                    &ctx->keys16, &ctx->finscr, &ctx->res, &ctx->akeys,
+                    &ctx->asums, &ctx->sums2})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -826,9 +857,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   // map device event times onto the host clock of the ChunkTiming fields
   CKR(cudaEventSynchronize(ev0));
   const double t_ev0 = since();
-  std::vector<uint32_t> skeys;
-  std::vector<int64_t> ssums;
-  std::vector<size_t> starts{0};
+  uint64_t sorted_n = 0;  // (key, sum) runs accumulated on the device
   std::vector<ecc_chunk_timing> tim(nchunks);
   std::vector<double> h2d_end_host(nchunks, 0);
   int rc = ECC_OK;
@@ -885,8 +914,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
     t.merge_begin = since();
     if (sorted) {
-      CKI(sorted_slab(ctx, s, st, &skeys, &ssums));
-      starts.push_back(skeys.size());
+      CKI(sorted_slab(ctx, s, st, dims.w0 * dims.w1 * dims.w2, &sorted_n));
     } else {
       CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
     }
@@ -918,7 +946,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
   BinResult r;
   if (sorted) {
     CKI(read_flags(ctx, st));
-    merge_runs(skeys, ssums, starts, &r);
+    CKI(sorted_finish(ctx, st, sorted_n, nchunks > 1, &r));
   } else {
     CKI(finalize_to_host(ctx, (uint32_t)nbins, st, &r));
   }
