@@ -37,7 +37,8 @@ from typing import List, Optional
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libecc_b200.so")
+# ECC_B200_LIB: load another build of the same library (variant experiments)
+LIB_PATH = os.environ.get("ECC_B200_LIB") or os.path.join(PKG, "lib", "libecc_b200.so")
 
 ECC_OK, ECC_EINVAL, ECC_ECUDA, ECC_ENOMEM, ECC_ESOURCE, ECC_EBINMAP, ECC_ENAN = 0, -1, -2, -3, -4, -5, -6
 ECC_U8, ECC_U16, ECC_F32 = 0, 1, 2

@@ -269,7 +269,22 @@ int read_flags(ecc_ctx* ctx, cudaStream_t st) {
 int pad_for_u8_fast(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine, cudaStream_t st,
                     Slab* out) {
   *out = s;
-  if (dtype != ECC_U8 || affine || s.w2 <= 1 || u8_3d_supported(s)) return ECC_OK;
+  if (dtype != ECC_U8 || affine) return ECC_OK;
+  if (s.w2 == 1) {  // 2D: rows along axis 1 padded to 16 bytes (k_u8_2d.cu)
+    if (u8_2d_supported(s)) return ECC_OK;
+    Slab p = s;
+    p.ppitch = (s.w1 + 15) / 16 * 16;
+    Slab probe = p;
+    probe.base = nullptr;
+    if (!u8_2d_supported(probe)) return ECC_OK;
+    CKI(ctx->pad.ensure((size_t)s.nplanes * p.ppitch));
+    CKR(cudaMemcpy2DAsync(ctx->pad.p, (size_t)p.ppitch, s.base, (size_t)s.plane_pitch(),
+                          (size_t)s.w1, (size_t)s.nplanes, cudaMemcpyDeviceToDevice, st));
+    p.base = ctx->pad.p;
+    *out = p;
+    return ECC_OK;
+  }
+  if (s.w2 <= 1 || u8_3d_supported(s)) return ECC_OK;
   Slab p = s;
   p.pitch = (s.w2 + 15) / 16 * 16;
   if (!u8_3d_supported(Slab{nullptr, p.plane0, p.nplanes, p.w0, p.w1, p.w2, p.own0, p.own1,
@@ -346,7 +361,7 @@ struct BinResult {
 
 // Whole 3D u8 image in ONE launch (k_u8_3d with the fused last-CTA K3).
 bool fusable(ecc_dtype dtype, const Slab& s, bool affine) {
-  return dtype == ECC_U8 && !affine && u8_3d_supported(s);
+  return dtype == ECC_U8 && !affine && (u8_3d_supported(s) || u8_2d_supported(s));
 }
 
 int launch_fused(ecc_ctx* ctx, const Slab& s, uint32_t* bins, int64_t* changes, int64_t* chi,
@@ -356,8 +371,11 @@ int launch_fused(ecc_ctx* ctx, const Slab& s, uint32_t* bins, int64_t* changes, 
     CKR(cudaMemsetAsync(ctx->fused.p, 0, 256 + 512 * 8, st));
   }
   U83dFinalize fz{ctx->fused.as<uint32_t>(), bins, changes, chi, count};
-  CKR(launch_u8_3d(s, reinterpret_cast<int64_t*>(ctx->fused.as<uint8_t>() + 256), nullptr,
-                   ctx->sms, st, &fz));
+  int64_t* ghist = reinterpret_cast<int64_t*>(ctx->fused.as<uint8_t>() + 256);
+  if (s.w2 == 1)
+    CKR(launch_u8_2d(s, ghist, ctx->sms, st, &fz));
+  else
+    CKR(launch_u8_3d(s, ghist, nullptr, ctx->sms, st, &fz));
   ctx->launches += 1;
   return ECC_OK;
 }

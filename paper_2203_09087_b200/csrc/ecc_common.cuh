@@ -157,7 +157,9 @@ struct Slab {
   int64_t w0, w1, w2;
   int64_t own0, own1;
   int64_t pitch = 0;  // elements between consecutive rows in memory (0 = w2)
+  int64_t ppitch = 0; // elements between consecutive planes (0 = w1 * row_pitch())
   __host__ __device__ int64_t row_pitch() const { return pitch ? pitch : w2; }
+  __host__ __device__ int64_t plane_pitch() const { return ppitch ? ppitch : w1 * row_pitch(); }
 };
 
 }  // namespace eccb

@@ -21,6 +21,9 @@ struct U83dFinalize {
 };
 bool u8_3d_supported(const Slab& s);
 bool u16_3d_supported(const Slab& s);
+bool u8_2d_supported(const Slab& s);
+cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st,
+                         const U83dFinalize* fz = nullptr);
 cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms, cudaStream_t st);
 cudaError_t launch_affine_keys(const float* v, uint64_t rows, uint32_t w2, uint32_t pitch,
                                const AffineMap& am, uint16_t* keys, uint32_t* flags, int sms,

@@ -1,5 +1,5 @@
-// k_fast.cu -- dispatch of u8 slabs to the bit-sliced TMA kernel
-// (k_u8_3d.cu); returns handled = false when the generic kernel
+// k_fast.cu -- dispatch of u8 slabs to the bit-sliced kernels
+// (k_u8_3d.cu, k_u8_2d.cu); returns handled = false when the generic kernel
 // (k_generic.cu) must run.  16-bit keys are dispatched in capi.cu
 // (accumulate_keys16), since they may need a conversion pass first.
 #include "internal.h"
@@ -16,6 +16,10 @@ cudaError_t launch_accumulate_fast(const Slab& s, int dtype, bool affine,
   if (dtype == 0 && !affine && nbins == 256 && u8_3d_supported(s)) {
     *handled = true;
     return launch_u8_3d(s, ghist, nullptr, sms, st);
+  }
+  if (dtype == 0 && !affine && nbins == 256 && u8_2d_supported(s)) {
+    *handled = true;
+    return launch_u8_2d(s, ghist, sms, st);
   }
   return cudaSuccess;
 }

@@ -1,0 +1,254 @@
+// k_u8_2d.cu -- K1+K2 for single 2D u8 images (w2 == 1) on sm_100a:
+// bit-sliced stencil + per-CTA (code, value) shared-memory histogram, with
+// the optional fused K3 of fin_u8.cuh (the whole curve in one launch).
+//
+// Replaces, for 2D u8 images, the reference hot loop
+//   run_chunk_kernel_u8 (streaming.hpp:146-174)
+//     -> accumulate_dense_u8 (kernel.hpp:268-277)
+//     -> for_each_change / change_2d (kernel.hpp:81-94, 193-216)
+// and produces the same per-value change sums and pixel counts bit-exactly.
+//
+// Mapping.  Rows run along axis 0, pixels of a row along axis 1.  A lane
+// owns a 32-pixel chunk of a row (bit p = pixel 32c + p) and a warp holds 32
+// consecutive chunks of the same row; lanes 0 and 31 are halo, so a warp
+// "strip" is 30 chunks (960 pixels) wide.  A work unit is (band of rows,
+// strip), band-major, so warps running together read neighbouring strips of
+// the same rows and the halo chunks / rows hit in L2.  The warp sweeps its
+// band row by row (one row prefetched ahead, two 16-byte loads per lane).
+//
+// Stencil (the 2D form of the tournament in k_u8_3d.cu, as in
+// k_batch16.cu).  Ties go to the earlier pixel (kernel.hpp:21-27):
+//   pairs along axis 1: gz = [c(p) > c(p+1)], pair minimum mz;
+//   pairs along axis 0: gx = [P(p) > N(p)] between consecutive rows;
+//   2 x 2 quads:        gq = [mz of row X-1 > mz of row X];
+// a pixel of row X-1 changes chi by 1 + #quads won - #pairs won, range
+// [-3, 1].  S = change + 3 (8 win bits through a small carry-save adder) is
+// the code; the three code planes are transposed back to bytes and every
+// pixel does ONE shared-memory red at hist[code][value].  Pixels the lane
+// does not emit get code 15.
+//
+// Collar.  Pixels outside the image hold 255; only an outside pixel on the
+// EARLIER side of a comparison is wrong (the reference's sentinel 256 must
+// lose), and those comparisons are forced: row -1 never wins (gx = gq =
+// FULL), column -1 never wins (the first chunk's left pair / quad).
+#include <algorithm>
+#include <cstdint>
+
+#include "bits.cuh"
+#include "ecc_common.cuh"
+#include "fin_u8.cuh"
+#include "internal.h"
+
+namespace eccb {
+namespace u82d {
+
+constexpr int NW = 8;  // warps per CTA
+constexpr int NT = NW * 32;
+constexpr int NCODE = 16;
+constexpr int HIST_WORDS = NCODE * 256;
+constexpr int CTAS_PER_SM = 2;
+constexpr int STRIP = 30;  // owned chunks per warp
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+
+struct Geom {
+  const uint8_t* base;  // row plane0 of the slab
+  long long pitch;      // bytes between rows (multiple of 16)
+  int W0, W1;           // image rows, pixels per row
+  int plane0;           // image row held at base
+  int own0, P;          // first owned row, owned rows
+  int nchunks;          // 32-pixel chunks per row
+  int nstrips;          // warps across a row
+  int band;             // rows per unit
+  int nunits;           // bands * nstrips
+  uint32_t four;        // = 4, opaque to ptxas (IMAD address, not an ALU LEA)
+};
+
+struct Codes {
+  static constexpr int n = 5;  // S = change + 3 in [0, 4]
+  static __device__ __forceinline__ bool live(int) { return true; }
+  static __device__ __forceinline__ int change(int c) { return c - 3; }
+};
+
+struct Row {
+  uint32_t C[8], mz[8];  // value planes, axis-1 pair minima
+  uint32_t gz;           // "right pixel wins" bits of the axis-1 pairs
+  uint32_t W[8];         // the chunk's 32 value bytes (natural order)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_u8_2d(const Geom g, int64_t* __restrict__ ghist, const u8fin::Fin fin) {
+  __shared__ __align__(16) uint32_t hist[HIST_WORDS];
+  for (int i = threadIdx.x; i < HIST_WORDS; i += NT) hist[i] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwt = gridDim.x * NW;
+  const uint32_t hist_s = smem_u32(hist);
+
+  for (int u = blockIdx.x * NW + warp; u < g.nunits; u += nwt) {
+    const int bi = u / g.nstrips, strip = u - bi * g.nstrips;
+    const int R0 = g.own0 + bi * g.band;
+    const int rows = min(g.band, g.own0 + g.P - R0);
+    const int c = strip * STRIP - 1 + lane;  // this lane's chunk (may be -1 or >= nchunks)
+    const int lo = 32 * c;
+    uint32_t zout = FULL;  // pixels of the chunk outside [0, W1)
+    if (c >= 0 && c < g.nchunks) zout = (g.W1 - lo >= 32) ? 0u : (FULL << (g.W1 - lo));
+    const uint32_t vm = (lane >= 1 && lane <= STRIP) ? ~zout : 0u;
+    const bool first = c == 0;
+    const bool chunk_in = c >= 0 && c < g.nchunks;
+    const bool hi_in = lo + 16 < g.W1;  // the chunk's second 16 bytes hold image pixels
+
+    auto load_row = [&](int i, uint32_t (&W)[8]) {
+      if (i < 0 || i >= g.W0 || !chunk_in) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) W[j] = FULL;
+        return;
+      }
+      const uint8_t* p = g.base + (long long)(i - g.plane0) * g.pitch + lo;
+      const uint4 a = ldg_stream(p);
+      W[0] = a.x; W[1] = a.y; W[2] = a.z; W[3] = a.w;
+      if (hi_in) {
+        const uint4 b = ldg_stream(p + 16);
+        W[4] = b.x; W[5] = b.y; W[6] = b.z; W[7] = b.w;
+      } else {
+        W[4] = W[5] = W[6] = W[7] = FULL;
+      }
+    };
+
+    Row A, B;
+    uint32_t xgx = 0, xgq = 0, xgq1 = 0;  // the previous row pair's results
+    uint32_t nxt[8];
+    load_row(R0 - 1, nxt);
+    // rows R0-1 .. R0+rows arrive; at the arrival of row X the changes of row
+    // X-1 are emitted (X-1 in [R0, R0 + rows), inside the image)
+    auto step = [&](int X, Row& P, Row& N, auto kind) {
+      constexpr int K = decltype(kind)::value;  // 0 first, 1 no emission, 2 emit
+#pragma unroll
+      for (int j = 0; j < 8; ++j) N.W[j] = nxt[j];
+      load_row(X + 1, nxt);  // prefetch
+      uint32_t (&C)[8] = N.C;
+      bits::byte_interleave(N.W, C);
+      bits::transpose8(C);
+      const uint32_t om = (X < 0 || X >= g.W0) ? FULL : zout;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) C[i] |= om;
+      {
+        uint32_t t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = __funnelshift_r(C[i], __shfl_down_sync(FULL, C[i], 1), 1);
+        N.gz = bits::gt<8>(C, t);
+        bits::sel<8>(N.mz, N.gz, C, t);
+      }
+      if constexpr (K >= 1) {
+        uint32_t gx = bits::gt<8>(P.C, N.C);
+        uint32_t gq = bits::gt<8>(P.mz, N.mz);
+        if (X - 1 < 0) gx = gq = FULL;  // row -1 never wins
+        // the quad anchored one pixel to the left: from the previous chunk,
+        // or for chunk 0 the quad over the left collar, whose minima are the
+        // pixels at 0 -- its comparison is gx bit 0
+        uint32_t qprev = __shfl_up_sync(FULL, gq, 1);
+        if (first) qprev = gx << 31;
+        const uint32_t gq1 = __funnelshift_l(qprev, gq, 1);
+        if constexpr (K == 2) {
+          const uint32_t vmr = (X - 1 < g.W0) ? vm : 0u;
+          uint32_t zprev = __shfl_up_sync(FULL, P.gz, 1);
+          if (first) zprev = FULL;  // column -1 never wins
+          if (vmr) {
+            const uint32_t Z0 = ~P.gz;
+            const uint32_t Z1 = __funnelshift_l(zprev, P.gz, 1);
+            // S = 4 quads won + 4 negated pairs won = change + 3
+            const uint32_t t0 = Z0 & ~gq, t1 = Z0 & xgq, t2 = Z1 & ~gq1, t3 = Z1 & xgq1;
+            const uint32_t t4 = ~Z0, t5 = ~Z1, t6 = gx, t7 = ~xgx;
+            uint32_t s0, c0, s1, c1, s2, c2;
+            bits::fa3(t0, t1, t2, s0, c0);
+            bits::fa3(t3, t4, t5, s1, c1);
+            bits::fa3(t6, t7, s0, s2, c2);
+            const uint32_t b0 = s1 ^ s2, k0 = s1 & s2;  // weight 1
+            uint32_t b1, k1;
+            bits::fa3(c0, c1, c2, b1, k1);              // weight 2
+            const uint32_t b1x = b1 ^ k0, k1x = b1 & k0;
+            const uint32_t b2 = k1 ^ k1x;               // weight 4 (S <= 4)
+            const uint32_t nv = ~vmr;
+            uint32_t V[8];
+            bits::transpose_codes(b0 | nv, b1x | nv, b2 | nv, nv, V);
+#pragma unroll
+            for (int p = 0; p < 32; ++p) {
+              const int r = p & 7, b = p >> 3;
+              const uint32_t idx = bits::prmt(
+                  P.W[p >> 2], V[r], (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
+              uint32_t addr;
+              asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(idx), "r"(g.four), "r"(hist_s));
+              asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+            }
+          }
+        }
+        xgx = gx;
+        xgq = gq;
+        xgq1 = gq1;
+      }
+    };
+    step(R0 - 1, B, A, std::integral_constant<int, 0>{});
+    step(R0, A, B, std::integral_constant<int, 1>{});
+    int X = R0 + 1;
+    for (; X + 1 <= R0 + rows; X += 2) {
+      step(X, B, A, std::integral_constant<int, 2>{});
+      step(X + 1, A, B, std::integral_constant<int, 2>{});
+    }
+    if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
+  }
+  u8fin::flush_and_finalize<NT, Codes>(hist, ghist, fin);
+}
+
+}  // namespace u82d
+
+bool u8_2d_supported(const Slab& s) {
+  return s.w2 == 1 && s.w1 >= 1 && s.plane_pitch() % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(s.base) % 16) == 0 && s.w0 < (1ll << 31) &&
+         s.w1 < (1ll << 31) - 64 && (s.own1 - s.own0) * s.w1 < (1ll << 40);
+}
+
+cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st,
+                         const U83dFinalize* fz) {
+  using namespace u82d;
+  Geom g;
+  g.base = static_cast<const uint8_t*>(s.base);
+  g.pitch = s.plane_pitch();
+  g.W0 = (int)s.w0;
+  g.W1 = (int)s.w1;
+  g.plane0 = (int)s.plane0;
+  g.own0 = (int)s.own0;
+  g.P = (int)(s.own1 - s.own0);
+  g.nchunks = (g.W1 + 31) / 32;
+  g.nstrips = (g.nchunks + STRIP - 1) / STRIP;
+  g.four = 4;
+  const long long cap_warps = (long long)sms * CTAS_PER_SM * NW;
+  // bands of >= 32 rows (2 halo rows per band); ~4 units per resident warp
+  // when the image is large enough, else one wave of shorter bands (>= 8)
+  long long nb = std::max<long long>(1, (4 * cap_warps) / g.nstrips);
+  long long band = std::max<long long>(32, (g.P + nb - 1) / nb);
+  if ((long long)((g.P + band - 1) / band) * g.nstrips < cap_warps)
+    band = std::max<long long>(8, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
+  band = std::max<long long>(1, std::min<long long>(band, std::max(1, g.P)));
+  g.band = (int)band;
+  const long long units = (g.P + band - 1) / band * g.nstrips;
+  if (g.P <= 0 || units > (1ll << 30)) return cudaErrorInvalidValue;
+  g.nunits = (int)units;
+  const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
+  u8fin::Fin fin{};
+  if (fz) fin = u8fin::Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+  k_u8_2d<<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
+  return cudaGetLastError();
+}
+
+}  // namespace eccb

@@ -52,10 +52,12 @@
 
 #include "bits.cuh"
 #include "ecc_common.cuh"
+#include "fin_u8.cuh"
 #include "internal.h"
 
 namespace eccb {
 namespace u83d {
+using u8fin::flush_and_finalize;
 
 constexpr int NW = 4;      // warps per CTA
 constexpr int NS = 4;      // TMA ring stages per warp
@@ -83,16 +85,9 @@ struct Geom {
   uint32_t four;   // = 4, opaque to ptxas so the histogram address stays an IMAD
 };
 
-// Fused K3 (optional): the last CTA to finish turns the global histogram
-// into the curve (merge_local + vcec_to_ecc, vcec.hpp:35-66, curve.hpp:28-35)
-// and re-zeroes the histogram and the ticket for the next launch.
-struct Fin {
-  uint32_t* ticket;    // zero before the launch, zero again after it
-  uint32_t* bins;      // [256] occurring values, ascending
-  int64_t* changes;    // [256] their VCEC entries
-  int64_t* chi;        // [256] the curve
-  uint64_t* count;     // number of occurring values
-};
+// Fused K3 (optional, fin_u8.cuh): the last CTA to finish turns the global
+// histogram into the curve.
+using u8fin::Fin;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -205,6 +200,13 @@ struct RunGeom {
 __device__ __forceinline__ int decode_change(uint32_t code) {
   return code >= 10 ? (int)code - 17 : (int)code - 1;
 }
+
+// code = (change + 17) mod 16; 8 = not emitted
+struct Codes {
+  static constexpr int n = NCODE;
+  static __device__ __forceinline__ bool live(int c) { return c != 8; }
+  static __device__ __forceinline__ int change(int c) { return decode_change((uint32_t)c); }
+};
 
 // One plane step of a column: plane X arrives as row N, row P holds plane
 // X-1.  KIND 0: the unit's first (halo) plane, tournament only; KIND 1: +
@@ -398,62 +400,7 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
     if (X <= x0 + len)
       sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
   }
-  if constexpr (!CH) {
-    __syncthreads();
-    // per value: change sum and voxel count over the codes (8 = not emitted)
-    for (int v = threadIdx.x; v < 256; v += NW * 32) {
-      long long sum = 0, cnt = 0;
-#pragma unroll
-      for (int c = 0; c < NCODE; ++c) {
-        if (c == 8) continue;
-        const long long n = hist[c * 256 + v];
-        cnt += n;
-        sum += n * decode_change((uint32_t)c);
-      }
-      if (cnt != 0) {
-        if (sum != 0)
-          atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[v]),
-                    static_cast<unsigned long long>(sum));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[256 + v]),
-                  static_cast<unsigned long long>(cnt));
-      }
-    }
-    if (fin.ticket) {
-      __shared__ bool last;
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) last = atomicAdd(fin.ticket, 1u) == gridDim.x - 1;
-      __syncthreads();
-      if (last) {
-        __threadfence();
-        // thread t owns values 2t, 2t+1
-        using Scan = cub::BlockScan<longlong2, NW * 32>;
-        __shared__ typename Scan::TempStorage tmp;
-        const int v0 = 2 * threadIdx.x;
-        const long long s0 = __ldcg(&ghist[v0]), s1 = __ldcg(&ghist[v0 + 1]);
-        const long long n0 = __ldcg(&ghist[256 + v0]), n1 = __ldcg(&ghist[256 + v0 + 1]);
-        longlong2 in = make_longlong2((n0 != 0) + (n1 != 0), s0 + s1), ex, total;
-        struct Add {
-          __device__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
-            return make_longlong2(a.x + b.x, a.y + b.y);
-          }
-        };
-        Scan(tmp).ExclusiveScan(in, ex, make_longlong2(0, 0), Add(), total);
-        long long pos = ex.x, acc = ex.y;
-        acc += s0;
-        if (n0 != 0) {
-          fin.bins[pos] = v0; fin.changes[pos] = s0; fin.chi[pos] = acc; ++pos;
-        }
-        acc += s1;
-        if (n1 != 0) {
-          fin.bins[pos] = v0 + 1; fin.changes[pos] = s1; fin.chi[pos] = acc;
-        }
-        if (threadIdx.x == 0) *fin.count = (uint64_t)total.x;
-        ghist[v0] = 0; ghist[v0 + 1] = 0; ghist[256 + v0] = 0; ghist[256 + v0 + 1] = 0;
-        if (threadIdx.x == 0) *fin.ticket = 0;
-      }
-    }
-  }
+  if constexpr (!CH) flush_and_finalize<NW * 32, Codes>(hist, ghist, fin);
 }
 
 }  // namespace u83d
