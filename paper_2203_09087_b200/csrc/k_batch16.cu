@@ -16,7 +16,6 @@
 // (range [-3, 1]).  The 8 win bits go through a small
 // carry-save adder; the result minus 3 is the change in 4-bit two's
 // complement, transposed back to signed bytes for the histogram.
-#include <cub/cub.cuh>
 #include <type_traits>
 
 #include "bits.cuh"
@@ -227,32 +226,63 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
   __syncthreads();
-  // epilogue: thread t owns bins [t * 128, (t + 1) * 128)
-  constexpr uint32_t per = 65536 / NT;
-  const uint32_t b0 = threadIdx.x * per;
+  // epilogue, conflict-free: warp w owns bins [w * 4096, (w + 1) * 4096) in
+  // 32 chunks of 128; lane l holds 4 consecutive bins of a chunk (one 8-byte
+  // shared load, the chunk's spill bits one broadcast word).  Pass 1 sums the
+  // warp's bins, pass 2 scans chunk by chunk and writes chi coalesced.
+  constexpr uint32_t PER_WARP = 65536 / NW;
   int32_t* row = chi + (size_t)blockIdx.x * 65536;
-  auto bin_sum = [&](uint32_t b) -> int {
-    int s = (int)((hw[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
-    if ((spilled[b >> 5] >> (b & 31)) & 1u) s += scratch[b];
-    return s;
+  auto sums4 = [&](uint32_t b, int (&x)[4]) {  // b % 4 == 0
+    const uint2 w2 = *reinterpret_cast<const uint2*>(hw + (b >> 1));
+    x[0] = (int)(w2.x & 0xFFFFu) - 32768;
+    x[1] = (int)(w2.x >> 16) - 32768;
+    x[2] = (int)(w2.y & 0xFFFFu) - 32768;
+    x[3] = (int)(w2.y >> 16) - 32768;
+    const uint32_t sp = (spilled[b >> 5] >> (b & 31)) & 0xFu;
+    if (sp) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((sp >> k) & 1u) x[k] += scratch[b + k];
+    }
   };
-  int32_t local = 0;
-  for (uint32_t b = b0; b < b0 + per; ++b) local += bin_sum(b);
-  using Scan = cub::BlockScan<int32_t, NT>;
-  __shared__ typename Scan::TempStorage tmp;
-  int32_t ex;
-  Scan(tmp).ExclusiveSum(local, ex);
-  for (uint32_t b = b0; b < b0 + per; b += 4) {
-    int4 o;
-    ex += bin_sum(b); o.x = ex;
-    ex += bin_sum(b + 1); o.y = ex;
-    ex += bin_sum(b + 2); o.z = ex;
-    ex += bin_sum(b + 3); o.w = ex;
-    *reinterpret_cast<int4*>(row + b) = o;
+  __shared__ int32_t wsum[NW];
+  const uint32_t wb = (uint32_t)warp * PER_WARP + 4u * lane;
+  int32_t part = 0;
+  for (uint32_t i = 0; i < PER_WARP; i += 128) {
+    int x[4];
+    sums4(wb + i, x);
+    part += x[0] + x[1] + x[2] + x[3];
+  }
+  part = __reduce_add_sync(FULL, part);
+  if (lane == 0) wsum[warp] = part;
+  __syncthreads();
+  int32_t carry = 0;
+  for (int j = 0; j < warp; ++j) carry += wsum[j];
+  for (uint32_t i = 0; i < PER_WARP; i += 128) {
+    int x[4];
+    sums4(wb + i, x);
+    x[1] += x[0];
+    x[2] += x[1];
+    x[3] += x[2];
+    int t = x[3];  // inclusive scan of the lane totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, t, o);
+      if (lane >= o) t += y;
+    }
+    const int base = carry + t - x[3];
+    *reinterpret_cast<int4*>(row + wb + i) = make_int4(base + x[0], base + x[1], base + x[2], base + x[3]);
+    carry += __shfl_sync(FULL, t, 31);
   }
   __syncthreads();  // every read of the scratch row is done
-  for (uint32_t b = b0; b < b0 + per; ++b)
-    if ((spilled[b >> 5] >> (b & 31)) & 1u) scratch[b] = 0;
+  for (int q = threadIdx.x; q < PWORDS; q += NT) {
+    uint32_t m = spilled[q];
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      scratch[q * 32 + bit] = 0;
+    }
+  }
   uint32_t* pres_row = presence + (size_t)blockIdx.x * PWORDS;
   for (int q = threadIdx.x; q < PWORDS; q += NT) pres_row[q] = pres[q];
 }
