@@ -30,12 +30,12 @@ __device__ __forceinline__ void issue(uint32_t hbase, uint32_t key, uint32_t chu
   u.key = key;
   u.mult = 1u + 65535u * (key & 1u);  // 1 or 65536: low or high half
   u.add = chu * u.mult;
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tmov.u32 %0, %4;\n\t"
-      "@q atom.shared.add.u32 %0, [%2], %3;\n\t}"
-      : "=r"(u.old)
-      : "r"(chu), "r"(hbase + ((key << 1) & ~3u)), "r"(u.add), "n"(BIAS)
-      : "memory");
+  // unconditional: a zero add is cheaper than the branch ptxas makes of a
+  // predicated atomic with a return value (ISETP + BSSY + BRA + BSYNC)
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+               : "=r"(u.old)
+               : "r"(hbase + ((key << 1) & ~3u)), "r"(u.add)
+               : "memory");
 }
 
 __device__ __forceinline__ uint32_t crossed(const Upd& u) {
