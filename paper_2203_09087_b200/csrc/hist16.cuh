@@ -56,16 +56,13 @@ __device__ __forceinline__ void fix(uint32_t hbase, const Upd& u, uint32_t cross
   }
 }
 
-// occupancy bit of `key` when `own` (set only if not set yet)
+// occupancy bit of `key` when `own` (0 or 1): an unconditional shared OR
+// (OR-ing 0 is a no-op); cheaper than testing the bit first, which ptxas
+// turns into a load, a compare and a branch per pixel.
 __device__ __forceinline__ void mark(uint32_t pbase, uint32_t key, uint32_t own) {
   const uint32_t pa = pbase + ((key >> 3) & ~3u);
-  const uint32_t bit = 1u << (key & 31);
-  uint32_t pw;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(pw) : "r"(pa) : "memory");
-  const uint32_t need = own & (uint32_t)((pw & bit) == 0);
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q red.shared.or.b32 [%1], %2;\n\t}" ::"r"(need),
-               "r"(pa), "r"(bit)
-               : "memory");
+  const uint32_t bit = own << (key & 31);
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(pa), "r"(bit) : "memory");
 }
 
 }  // namespace hist16
