@@ -298,8 +298,8 @@ int pad_for_u8_fast(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine, c
   return ECC_OK;
 }
 
-// 3D u16 volumes and affine-quantised f32 volumes with <= 65536 bins run the
-// 16-bit bit-sliced kernel (k_u16_3d.cu): f32 slabs are first mapped to bin
+// u16 images and affine-quantised f32 images with <= 65536 bins run the
+// 16-bit bit-sliced kernels (k_u16_3d.cu, k_u16_2d.cu): f32 slabs are first mapped to bin
 // indices (monotone, so the stencil sees the same order), u16 slabs whose
 // rows break the 16-byte TMA stride rule are copied to a padded pitch.
 int accumulate_keys16(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine,
@@ -308,8 +308,30 @@ int accumulate_keys16(ecc_ctx* ctx, const Slab& s, ecc_dtype dtype, bool affine,
   *handled = false;
   const bool u16 = dtype == ECC_U16 && !affine && nbins == 65536;
   const bool f32 = dtype == ECC_F32 && affine && nbins <= 65536;
-  if (s.w2 <= 1 || !(u16 || f32) || s.w1 > (1 << 30) || s.w2 > (1 << 30) || s.w0 > (1 << 30))
+  if (!(u16 || f32) || s.w1 > (1 << 30) || s.w2 > (1 << 30) || s.w0 > (1 << 30)) return ECC_OK;
+  if (s.w2 == 1) {  // 2D (k_u16_2d.cu): rows along axis 1, pitch a multiple of 8 keys
+    Slab k = s;
+    if (f32 || !u16_2d_supported(s)) {
+      k.ppitch = (s.w1 + 7) / 8 * 8;
+      CKI(ctx->keys16.ensure((size_t)s.nplanes * k.ppitch * 2));
+      if (f32) {
+        CKR(launch_affine_keys(static_cast<const float*>(s.base), (uint64_t)s.nplanes,
+                               (uint32_t)s.w1, (uint32_t)k.ppitch, am, ctx->keys16.as<uint16_t>(),
+                               ctx->flags.as<uint32_t>(), ctx->sms, st));
+        ctx->launches += 1;
+      } else {
+        CKR(cudaMemcpy2DAsync(ctx->keys16.p, (size_t)k.ppitch * 2, s.base,
+                              (size_t)s.plane_pitch() * 2, (size_t)s.w1 * 2, (size_t)s.nplanes,
+                              cudaMemcpyDeviceToDevice, st));
+      }
+      k.base = ctx->keys16.p;
+    }
+    CKR(launch_u16_2d(k, nbins, hist, ctx->sms, st));
+    ctx->launches += 1;
+    *handled = true;
     return ECC_OK;
+  }
+  if (s.w2 < 1) return ECC_OK;
   Slab k = s;
   if (f32 || !u16_3d_supported(s)) {
     k.pitch = (s.w2 + 7) / 8 * 8;

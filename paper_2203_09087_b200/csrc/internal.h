@@ -22,6 +22,8 @@ struct U83dFinalize {
 bool u8_3d_supported(const Slab& s);
 bool u16_3d_supported(const Slab& s);
 bool u8_2d_supported(const Slab& s);
+bool u16_2d_supported(const Slab& s);
+cudaError_t launch_u16_2d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms, cudaStream_t st);
 cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st,
                          const U83dFinalize* fz = nullptr);
 cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms, cudaStream_t st);

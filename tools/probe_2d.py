@@ -20,3 +20,14 @@ for shape, dt in [((8192, 8192), torch.uint8), ((6400, 3200), torch.uint8), ((81
     b.record(st); torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 10
     print(shape, dt, round(ms, 3), "ms", round(img.numel() / ms / 1e6, 1), "GVox/s", flush=True)
+# 2D affine-quantised f32 (65536 levels)
+img = torch.empty((8192, 8192), dtype=torch.float32, device="cuda")
+ctx.fill_synthetic(img, seed=1)
+bm = eb.quantised_binmap(65536)
+ctx.vcec(img, binmap=bm)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record(st)
+for _ in range(5): ctx.vcec(img, binmap=bm)
+b.record(st); torch.cuda.synchronize()
+print("(8192, 8192) f32 affine 65536 vcec (incl. result copy):", round(a.elapsed_time(b) / 5, 3), "ms", flush=True)
