@@ -7,3 +7,4 @@
 #include "ecc/curve.hpp"
 #include "ecc/device.hpp"
 #include "ecc/streaming.hpp"
+#include "ecc/pipeline.hpp"

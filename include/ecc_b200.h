@@ -223,6 +223,36 @@ ECC_API int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dty
 ECC_API int ecc_fill_synthetic(ecc_ctx* ctx, void* d_data, ecc_dtype dtype,
                        uint64_t n, uint64_t seed, uint64_t base, void* stream);
 
+/* ------------------------------------------------------------ pipeline
+ * The reference's in-memory benchmark, GPU-resident.
+ *
+ * ecc_uniform_noise: d_out[i] = counter_uniform(seed, i) = (counter_hash(seed, i) >> 40) * 2^-24
+ *   (uniform_noise, datagen.hpp:57-62; counter_uniform :30-32), bit-identical.
+ * ecc_gaussian_smooth: separable Gaussian smoothing with a normalised sampled
+ *   kernel and edge clamping (gaussian_smooth datagen.hpp:108-122, convolve_axis
+ *   :80-105, gaussian_kernel :66-79), bit-identical floats; d_in may equal d_out.
+ *   Errors: "Gaussian kernel width must be odd and >= 1".
+ * ecc_bench_run: bench_run (pipeline.hpp:236-291): uniform noise once, then
+ *   `iterations` x {gaussian_smooth; process_image + vcec_to_ecc of the f32
+ *   volume on the sorted (exact) path}, everything in device memory.  The
+ *   report mirrors BenchReport (pipeline.hpp:212-233); smoothing / ECC times
+ *   are CUDA-event device times, generate / total host wall time.  Errors:
+ *   "bench needs at least one iteration". */
+typedef struct {
+  uint64_t iterations, voxels;
+  double generate_s, total_s, per_iteration_s, ecc_avg_s, smooth_avg_s, ecc_gvox_per_s;
+  uint64_t last_points;    /* points of the last iteration's curve */
+  int64_t last_chi_first;  /* its chi at the lowest threshold */
+  int64_t last_chi_last;   /* and at the highest (1 for any non-empty image) */
+} ecc_bench_report;
+
+ECC_API int ecc_uniform_noise(ecc_ctx* ctx, float* d_out, uint64_t n, uint64_t seed,
+                              void* stream);
+ECC_API int ecc_gaussian_smooth(ecc_ctx* ctx, const float* d_in, float* d_out, ecc_dims dims,
+                                double sigma, int width, void* stream);
+ECC_API int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t seed,
+                          double sigma, int width, ecc_bench_report* report);
+
 #ifdef __cplusplus
 }
 #endif

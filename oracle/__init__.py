@@ -64,6 +64,10 @@ def lib():
         L.ecc_oracle_float_order_key.restype = C.c_uint32
         L.ecc_oracle_float_from_order_key.argtypes = [C.c_uint32]
         L.ecc_oracle_float_from_order_key.restype = C.c_float
+        L.ecc_oracle_uniform_noise.argtypes = [_vp, _u64, _u64]
+        L.ecc_oracle_uniform_noise.restype = None
+        L.ecc_oracle_gaussian_smooth.argtypes = [_vp, _vp, _u64, _u64, _u64, C.c_double, C.c_int]
+        L.ecc_oracle_gaussian_smooth.restype = C.c_int
         _LIB = L
     return _LIB
 
@@ -92,6 +96,12 @@ def ref():
         for n in ("ref_curve_csv_u8", "ref_curve_csv_f32"):
             getattr(R, n).argtypes = [_vp, _vp, _u64, _vp, _u64]
             getattr(R, n).restype = _i64
+        R.ref_uniform_noise.argtypes = [_u64, _u64, _u64, _u64, _vp]
+        R.ref_uniform_noise.restype = None
+        R.ref_gaussian_smooth.argtypes = [_vp, _u64, _u64, _u64, C.c_double, C.c_int, _vp]
+        R.ref_gaussian_smooth.restype = C.c_int
+        R.ref_bench_run.argtypes = [_u64, _u64, _u64, _u64, _u64, C.c_double, C.c_int, _vp]
+        R.ref_bench_run.restype = C.c_int
         _REF = R
     return _REF
 
@@ -181,6 +191,52 @@ def hist_dense(img: np.ndarray):
 
 
 # ---------------------------------------------------------------- reference engine
+def uniform_noise(shape, seed: int) -> np.ndarray:
+    """uniform_noise (datagen.hpp:57-62) restated in C."""
+    out = np.empty(shape, np.float32)
+    lib().ecc_oracle_uniform_noise(_p(out), out.size, seed)
+    return out
+
+
+def gaussian_smooth(img: np.ndarray, sigma: float, width: int) -> np.ndarray:
+    """gaussian_smooth (datagen.hpp:108-122) restated in C."""
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    w0, w1, w2 = _dims3(img)
+    out = np.empty_like(img)
+    if lib().ecc_oracle_gaussian_smooth(_p(img), _p(out), w0, w1, w2, sigma, width) != 0:
+        raise ValueError("Gaussian kernel width must be odd and >= 1")
+    return out
+
+
+def ref_uniform_noise(shape, seed: int) -> np.ndarray:
+    w0, w1, w2 = (tuple(shape) + (1,))[:3] if len(shape) == 2 else tuple(shape)
+    out = np.empty(shape, np.float32)
+    ref().ref_uniform_noise(w0, w1, w2, seed, _p(out))
+    return out
+
+
+def ref_gaussian_smooth(img: np.ndarray, sigma: float, width: int) -> np.ndarray:
+    img = np.ascontiguousarray(img, dtype=np.float32)
+    w0, w1, w2 = _dims3(img)
+    out = np.empty_like(img)
+    R = ref()
+    if R.ref_gaussian_smooth(_p(img), w0, w1, w2, sigma, width, _p(out)) != 0:
+        raise ValueError(R.ref_last_error().decode())
+    return out
+
+
+def ref_bench_run(shape, iterations: int, seed: int = 1, sigma: float = 2.0, width: int = 13):
+    """bench_run (pipeline.hpp:236-291) through the compiled reference:
+    dict of its BenchReport timings."""
+    w0, w1, w2 = tuple(shape) if len(shape) == 3 else (shape[0], shape[1], 1)
+    r = np.zeros(6, np.float64)
+    R = ref()
+    if R.ref_bench_run(w0, w1, w2, iterations, seed, sigma, width, _p(r)) != 0:
+        raise ValueError(R.ref_last_error().decode())
+    keys = ("generate_s", "total_s", "per_iteration_s", "ecc_avg_s", "smooth_avg_s", "ecc_gvox_per_s")
+    return dict(zip(keys, map(float, r)))
+
+
 def ref_vcec(img: np.ndarray, chunks: int = 1, workers: int = 1, phases=None):
     """process_image through the compiled reference (u8 and f32 paths).
 

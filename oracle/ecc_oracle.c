@@ -254,3 +254,59 @@ void ecc_oracle_prefix_sum(const int64_t* changes, int64_t* chi, uint64_t m) {
   int64_t acc = 0;
   for (uint64_t i = 0; i < m; ++i) { acc += changes[i]; chi[i] = acc; }
 }
+
+/* ---------------------------------------------------------------------- */
+/* Pipeline inputs: uniform_noise datagen.hpp:57-62
+ * with counter_uniform :30-32; gaussian_smooth :108-122 = gaussian_kernel
+ * :66-79 + convolve_axis :80-105 along axes 0, 1, 2 (skipped when the axis
+ * extent or the width is 1), edge-clamped, double accumulation in tap order,
+ * rounded to float.  Built as ISO C (no FMA contraction), like the reference. */
+
+void ecc_oracle_uniform_noise(float* dst, uint64_t n, uint64_t seed) {
+  for (uint64_t i = 0; i < n; ++i)
+    dst[i] = (float)(ecc_oracle_counter_hash(seed, i) >> 40) * 0x1p-24f;
+}
+
+/* returns -1 for an invalid width (even or < 1) */
+int ecc_oracle_gaussian_smooth(const float* in, float* out, uint64_t w0, uint64_t w1,
+                               uint64_t w2, double sigma, int width) {
+  if (width < 1 || width % 2 == 0) return -1;
+  const int half = width / 2;
+  double* kern = (double*)malloc(sizeof(double) * (size_t)width);
+  double sum = 0;
+  for (int i = -half; i <= half; ++i) {
+    const double v = width == 1 ? 1.0 : exp(-((double)i * i) / (2.0 * sigma * sigma));
+    kern[i + half] = v;
+    sum += v;
+  }
+  for (int i = 0; i < width; ++i) kern[i] /= sum;
+  const uint64_t n = w0 * w1 * w2;
+  const uint64_t ext[3] = {w0, w1, w2};
+  const uint64_t stride[3] = {w1 * w2, w2, 1};
+  float* cur = (float*)malloc(sizeof(float) * (n ? n : 1));
+  float* nxt = (float*)malloc(sizeof(float) * (n ? n : 1));
+  memcpy(cur, in, sizeof(float) * n);
+  for (int axis = 0; axis < 3; ++axis) {
+    const uint64_t aw = ext[axis], as = stride[axis];
+    if (!(aw > 1 && width > 1)) continue;
+    for (uint64_t i = 0; i < n; ++i) {
+      const int64_t pos = (int64_t)((i / as) % aw);
+      double acc = 0;
+      for (int k = -half; k <= half; ++k) {
+        int64_t q = pos + k;
+        if (q < 0) q = 0;
+        if (q > (int64_t)aw - 1) q = (int64_t)aw - 1;
+        acc += kern[k + half] * (double)cur[i + (uint64_t)(q - pos) * as];
+      }
+      nxt[i] = (float)acc;
+    }
+    float* t = cur;
+    cur = nxt;
+    nxt = t;
+  }
+  memcpy(out, cur, sizeof(float) * n);
+  free(cur);
+  free(nxt);
+  free(kern);
+  return 0;
+}

@@ -18,6 +18,7 @@
 #include "ecc/curve.hpp"
 #include "ecc/datagen.hpp"
 #include "ecc/oracle.hpp"
+#include "ecc/pipeline.hpp"
 #include "ecc/streaming.hpp"
 
 namespace {
@@ -152,6 +153,49 @@ std::int64_t ref_curve_csv_u8(const std::uint8_t* t, const std::int64_t* chi,
 std::int64_t ref_curve_csv_f32(const float* t, const std::int64_t* chi,
                                std::uint64_t m, char* out, std::uint64_t cap) {
   return csv<float>(t, chi, m, out, cap);
+}
+
+// Pipeline pieces (datagen.hpp:57-62, 108-122; pipeline.hpp:236-291).
+void ref_uniform_noise(std::uint64_t w0, std::uint64_t w1, std::uint64_t w2,
+                       std::uint64_t seed, float* out) {
+  ecc::GenSpec spec;
+  spec.dims = {w0, w1, w2};
+  spec.seed = seed;
+  const auto img = ecc::uniform_noise(spec);
+  std::memcpy(out, img.values.data(), img.values.size() * sizeof(float));
+}
+
+int ref_gaussian_smooth(const float* in, std::uint64_t w0, std::uint64_t w1,
+                        std::uint64_t w2, double sigma, int width, float* out) {
+  try {
+    ecc::Image<float> im{{w0, w1, w2}, std::vector<float>(in, in + w0 * w1 * w2)};
+    const auto sm = ecc::gaussian_smooth(im, sigma, width);
+    std::memcpy(out, sm.values.data(), sm.values.size() * sizeof(float));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// bench_run; r = {generate_s, total_s, per_iteration_s, ecc_avg_s,
+// smooth_avg_s, ecc_gvox_per_s}
+int ref_bench_run(std::uint64_t w0, std::uint64_t w1, std::uint64_t w2,
+                  std::uint64_t iterations, std::uint64_t seed, double sigma,
+                  int width, double* r) {
+  try {
+    const auto rep = ecc::bench_run({w0, w1, w2}, iterations, seed, sigma, width);
+    r[0] = rep.generate_s;
+    r[1] = rep.total_s;
+    r[2] = rep.per_iteration_s;
+    r[3] = rep.ecc_avg_s;
+    r[4] = rep.smooth_avg_s;
+    r[5] = rep.ecc_gvox_per_s;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -69,6 +69,15 @@ class _Timing(C.Structure):
                 ("merge_begin", C.c_double), ("merge_end", C.c_double)]
 
 
+class _BenchReport(C.Structure):
+    _fields_ = [("iterations", C.c_uint64), ("voxels", C.c_uint64),
+                ("generate_s", C.c_double), ("total_s", C.c_double),
+                ("per_iteration_s", C.c_double), ("ecc_avg_s", C.c_double),
+                ("smooth_avg_s", C.c_double), ("ecc_gvox_per_s", C.c_double),
+                ("last_points", C.c_uint64), ("last_chi_first", C.c_int64),
+                ("last_chi_last", C.c_int64)]
+
+
 READ_ROWS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                            C.c_void_p, C.c_size_t)
 
@@ -115,10 +124,15 @@ def lib() -> C.CDLL:
                                              _vp, _vp, _u64, C.POINTER(_u64)]
             L.ecc_batch2d.argtypes = [_vp, _vp, C.c_int, C.c_int, _u64, _u64, _u64, _vp, _vp, _vp]
             L.ecc_fill_synthetic.argtypes = [_vp, _vp, C.c_int, _u64, _u64, _u64, _vp]
+            L.ecc_uniform_noise.argtypes = [_vp, _vp, _u64, _u64, _vp]
+            L.ecc_gaussian_smooth.argtypes = [_vp, _vp, _vp, _Dims, C.c_double, C.c_int, _vp]
+            L.ecc_bench_run.argtypes = [_vp, _Dims, _u64, _u64, C.c_double, C.c_int,
+                                        C.POINTER(_BenchReport)]
             for n in ("ecc_ctx_create", "ecc_bin_count", "ecc_accumulate_slab", "ecc_compute_changes",
                       "ecc_finalize", "ecc_vcec", "ecc_curve", "ecc_process_stream", "ecc_batch2d",
                       "ecc_fill_synthetic", "ecc_curve_device", "ecc_process_host",
-                      "ecc_process_file"):
+                      "ecc_process_file", "ecc_uniform_noise", "ecc_gaussian_smooth",
+                      "ecc_bench_run"):
                 getattr(L, n).restype = C.c_int
             _lib = L
         return _lib
@@ -280,6 +294,34 @@ class EngineReport:
     kernel_s: float = 0.0
     merge_s: float = 0.0
     peak_chunk_bytes: int = 0
+
+
+@dataclass
+class BenchReport:
+    """BenchReport (pipeline.hpp:212-233) of the GPU-resident bench_run, plus
+    the last iteration's curve summary."""
+    iterations: int = 0
+    voxels: int = 0
+    generate_s: float = 0.0
+    total_s: float = 0.0
+    per_iteration_s: float = 0.0
+    ecc_avg_s: float = 0.0
+    smooth_avg_s: float = 0.0
+    ecc_gvox_per_s: float = 0.0
+    last_points: int = 0
+    last_chi_first: int = 0
+    last_chi_last: int = 0
+
+    def to_string(self) -> str:
+        """Same lines as the reference's BenchReport::to_string."""
+        return (f"iterations:       {self.iterations}\n"
+                f"voxels:           {self.voxels}\n"
+                f"generate:         {self.generate_s:g} s\n"
+                f"loop total:       {self.total_s:g} s\n"
+                f"per iteration:    {self.per_iteration_s:g} s\n"
+                f"ECC avg:          {self.ecc_avg_s:g} s\n"
+                f"smoothing avg:    {self.smooth_avg_s:g} s\n"
+                f"ECC GVox/s:       {self.ecc_gvox_per_s:g}\n")
 
 
 @dataclass
@@ -609,6 +651,33 @@ class Context:
                                  chi.ctypes.data, presence.ctypes.data, None))
         return chi, presence
 
+    def uniform_noise(self, tensor, seed: int = 0, stream: int = 0):
+        """uniform_noise (datagen.hpp:57-62) into a device float32 tensor."""
+        _check(lib().ecc_uniform_noise(self._p, tensor.data_ptr(), tensor.numel(), seed,
+                                       stream or None))
+        return tensor
+
+    def gaussian_smooth(self, tensor, sigma: float, width: int, out=None, stream: int = 0):
+        """gaussian_smooth (datagen.hpp:108-122) of a device float32 tensor
+        (2D or 3D), bit-identical to the reference; out may be the input."""
+        import torch
+        if out is None:
+            out = torch.empty_like(tensor)
+        _check(lib().ecc_gaussian_smooth(self._p, tensor.data_ptr(), out.data_ptr(),
+                                         _dims_of(tuple(tensor.shape)), sigma, width,
+                                         stream or None))
+        return out
+
+    def bench_run(self, dims: Dims, iterations: int, seed: int = 1, sigma: float = 2.0,
+                  width: int = 13) -> BenchReport:
+        """bench_run (pipeline.hpp:236-291) on the GPU: uniform noise once, then
+        `iterations` x {gaussian_smooth; ECC on the exact f32 path}, all in
+        device memory."""
+        r = _BenchReport()
+        _check(lib().ecc_bench_run(self._p, _Dims(dims.w0, dims.w1, dims.w2), iterations, seed,
+                                   sigma, width, C.byref(r)))
+        return BenchReport(**{f: getattr(r, f) for f, _ in _BenchReport._fields_})
+
     def fill_synthetic(self, tensor, seed: int = 1, base: int = 0, stream: int = 0):
         import torch
         dt = {torch.uint8: ECC_U8, torch.uint16: ECC_U16, torch.float32: ECC_F32}[tensor.dtype]
@@ -657,6 +726,16 @@ def process_image(image, plan: ChunkPlan = None, options: EngineOptions = None,
             return ctx.process_host(arr, plan, report, binmap)
         return ctx.process_source(MemorySource(image), plan, options, report, binmap)
     return ctx.vcec(image, binmap)
+
+
+def _dims_of(shape) -> _Dims:
+    d = Dims.of(shape)
+    return _Dims(d.w0, d.w1, d.w2)
+
+
+def bench_run(dims: Dims, iterations: int, seed: int = 1, sigma: float = 2.0, width: int = 13,
+              device: int = 0) -> BenchReport:
+    return context(device).bench_run(dims, iterations, seed, sigma, width)
 
 
 def batch2d(images, **kw):

@@ -139,8 +139,9 @@ struct ecc_ctx {
   DevBuf finscr;    // K3 partials for large bin counts
   DevBuf res;       // result block (count, flags, curve) read back in one copy
   PinBuf res_host;
-  DevBuf keys16;
-  DevBuf akeys, asums, sums2;  // sorted f32 path: per-slab runs and their merge    // 16-bit keys (u16 padded / f32 bin indices) for k_u16_3d
+  DevBuf keys16;    // 16-bit keys (u16 padded / f32 bin indices) for the 16-bit kernels
+  DevBuf akeys, asums, sums2;  // sorted f32 path: per-slab runs and their merge
+  DevBuf sm_tmp[2], sm_w;     // gaussian_smooth: axis temporaries and the taps
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
 };
@@ -517,7 +518,10 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
 // merge_local (vcec.hpp:35-66) of every slab's runs on the device: one more
 // sort + reduce-by-key when there were several slabs, then the int64 prefix
 // sum (vcec_to_ecc) and one copy back.
-int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResult* out) {
+// out == nullptr: the curve stays on the device (keys in ctx->keys or
+// ctx->akeys, sums, chi in ctx->chi); *m_out gets the point count.
+int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResult* out,
+                  uint64_t* m_out = nullptr) {
   uint32_t* keys = ctx->akeys.as<uint32_t>();
   int64_t* sums = ctx->asums.as<int64_t>();
   uint64_t m = n;
@@ -558,6 +562,8 @@ int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResu
     CKR(cub::DeviceScan::InclusiveSum(ctx->tmp.p, t3, sums, ctx->chi.as<int64_t>(), (int)m, st));
     ctx->launches += 1;
   }
+  if (m_out) *m_out = m;
+  if (!out) return ECC_OK;
   out->keys.resize(m);
   out->changes.resize(m);
   out->chi.resize(m);
@@ -654,6 +660,61 @@ int batch_scratch(ecc_ctx* ctx, ecc_dtype dtype, cudaStream_t st) {
   return ECC_OK;
 }
 
+// gaussian_kernel (datagen.hpp:66-79), restated on the host with the same
+// double arithmetic and libm exp, so the taps are bit-identical.
+int gaussian_weights(double sigma, int width, std::vector<double>* w) {
+  if (width < 1 || width % 2 == 0)
+    return fail(ECC_EINVAL, "Gaussian kernel width must be odd and >= 1");
+  if (width > gaussian_max_width())
+    return fail(ECC_EINVAL, "Gaussian kernel width " + std::to_string(width) + " exceeds " +
+                                std::to_string(gaussian_max_width()));
+  w->assign(width, 0.0);
+  const int half = width / 2;
+  double sum = 0;
+  for (int i = -half; i <= half; ++i) {
+    const double v = width == 1 ? 1.0 : std::exp(-(double(i) * i) / (2.0 * sigma * sigma));
+    (*w)[i + half] = v;
+    sum += v;
+  }
+  for (double& v : *w) v /= sum;
+  return ECC_OK;
+}
+
+// gaussian_smooth (datagen.hpp:108-122): axes 0, 1, 2 in turn, each skipped
+// when its extent or the width is 1; in may equal out.
+int smooth_device(ecc_ctx* ctx, const float* in, float* out, ecc_dims d, double sigma, int width,
+                  cudaStream_t st) {
+  std::vector<double> w;
+  CKI(gaussian_weights(sigma, width, &w));
+  const uint64_t n = d.w0 * d.w1 * d.w2;
+  const uint64_t ext[3] = {d.w0, d.w1, d.w2};
+  int axes[3], na = 0;
+  for (int a = 0; a < 3; ++a)
+    if (ext[a] > 1 && width > 1) axes[na++] = a;
+  if (na == 0) {
+    if (in != out) CKR(cudaMemcpyAsync(out, in, n * 4, cudaMemcpyDeviceToDevice, st));
+    return ECC_OK;
+  }
+  CKI(ctx->sm_w.ensure(w.size() * 8));
+  CKR(cudaMemcpyAsync(ctx->sm_w.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, st));
+  CKI(ctx->sm_tmp[0].ensure(n * 4));
+  if (na > 2) CKI(ctx->sm_tmp[1].ensure(n * 4));
+  const float* src = in;
+  // in place with a single active axis: the pass must not write what it reads
+  const bool via_tmp = na == 1 && in == out;
+  for (int j = 0; j < na; ++j) {
+    float* dst = (j == na - 1 && !via_tmp) ? out : ctx->sm_tmp[j & 1].as<float>();
+    CKR(launch_convolve_axis(src, dst, d.w0, d.w1, d.w2, axes[j], ctx->sm_w.as<double>(), width,
+                             st));
+    ctx->launches += 1;
+    src = dst;
+  }
+  if (via_tmp) CKR(cudaMemcpyAsync(out, src, n * 4, cudaMemcpyDeviceToDevice, st));
+  // (a pageable-source async copy returns once the taps are staged, so `w`
+  // may go out of scope here)
+  return ECC_OK;
+}
+
 }  // namespace
 
 // ===================================================================== ABI
@@ -695,7 +756,7 @@ void ecc_ctx_destroy(ecc_ctx* ctx) {
                     &ctx->ch8b, &ctx->sums, &ctx->tmp, &ctx->slab[0], &ctx->slab[1], &ctx->slab[2],
                     &ctx->fused, &ctx->bscratch, &ctx->nanidx, &ctx->pad,
                     &ctx->keys16, &ctx->finscr, &ctx->res, &ctx->akeys,
-                    &ctx->asums, &ctx->sums2})
+                    &ctx->asums, &ctx->sums2, &ctx->sm_tmp[0], &ctx->sm_tmp[1], &ctx->sm_w})
     b->release();
   ctx->staging[0].release();
   ctx->staging[1].release();
@@ -1207,6 +1268,97 @@ int ecc_fill_synthetic(ecc_ctx* ctx, void* d_data, ecc_dtype dtype, uint64_t n,
   CKI(check_dtype(dtype));
   if (!d_data) return fail(ECC_EINVAL, "null device pointer");
   CKR(launch_fill(d_data, (int)dtype, n, seed, base, ctx->sms, pick(ctx, stream)));
+  return ECC_OK;
+}
+
+int ecc_uniform_noise(ecc_ctx* ctx, float* d_out, uint64_t n, uint64_t seed, void* stream) {
+  CKI(bind(ctx));
+  if (!d_out) return fail(ECC_EINVAL, "null device pointer");
+  CKR(launch_uniform_noise(d_out, n, seed, ctx->sms, pick(ctx, stream)));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+int ecc_gaussian_smooth(ecc_ctx* ctx, const float* d_in, float* d_out, ecc_dims dims,
+                        double sigma, int width, void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dims(dims));
+  if (!d_in || !d_out) return fail(ECC_EINVAL, "null device pointer");
+  return smooth_device(ctx, d_in, d_out, dims, sigma, width, pick(ctx, stream));
+}
+
+int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t seed, double sigma,
+                  int width, ecc_bench_report* rep) {
+  CKI(bind(ctx));
+  CKI(check_dims(dims));
+  if (!rep) return fail(ECC_EINVAL, "null report");
+  if (iterations < 1) return fail(ECC_EINVAL, "bench needs at least one iteration");
+  {
+    std::vector<double> w;
+    CKI(gaussian_weights(sigma, width, &w));
+  }
+  using clk = std::chrono::steady_clock;
+  const auto secs = [](clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
+  cudaStream_t st = ctx->stream;
+  const uint64_t n = dims.w0 * dims.w1 * dims.w2;
+  std::memset(rep, 0, sizeof(*rep));
+  rep->iterations = iterations;
+  rep->voxels = n;
+  CKI(ctx->input.ensure(n * 4));
+  float* img = ctx->input.as<float>();
+  CKI(ctx->flags.ensure(4));
+  const auto tg0 = clk::now();
+  CKR(launch_uniform_noise(img, n, seed, ctx->sms, st));
+  ctx->launches += 1;
+  CKR(cudaStreamSynchronize(st));
+  rep->generate_s = secs(tg0, clk::now());
+  cudaEvent_t e0, e1, e2;
+  CKR(cudaEventCreate(&e0));
+  CKR(cudaEventCreate(&e1));
+  CKR(cudaEventCreate(&e2));
+  double smooth_ms = 0, ecc_ms = 0;
+  uint64_t m = 0;
+  int rc = ECC_OK;
+  const Slab s = make_slab(img, dims, 0, dims.w0, 0, dims.w0);
+  const auto t0 = clk::now();
+  for (uint64_t it = 0; it < iterations && rc == ECC_OK; ++it) {
+    cudaEventRecord(e0, st);
+    rc = smooth_device(ctx, img, img, dims, sigma, width, st);
+    if (rc != ECC_OK) break;
+    cudaEventRecord(e1, st);
+    // process_image + vcec_to_ecc (streaming.hpp:332-338, curve.hpp:28-35)
+    // on the sorted f32 path; the curve stays in device memory
+    cudaMemsetAsync(ctx->flags.p, 0, 4, st);
+    uint64_t nacc = 0;
+    rc = sorted_slab(ctx, s, st, n, &nacc);
+    if (rc == ECC_OK) rc = read_flags(ctx, st);
+    if (rc == ECC_OK) rc = sorted_finish(ctx, st, nacc, false, nullptr, &m);
+    cudaEventRecord(e2, st);
+    cudaEventSynchronize(e2);
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, e0, e1);
+    cudaEventElapsedTime(&b, e1, e2);
+    smooth_ms += a;
+    ecc_ms += b;
+  }
+  rep->total_s = secs(t0, clk::now());
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  CKI(rc);
+  const double it = (double)iterations;
+  rep->per_iteration_s = (rep->generate_s + rep->total_s) / it;
+  rep->ecc_avg_s = ecc_ms * 1e-3 / it;
+  rep->smooth_avg_s = smooth_ms * 1e-3 / it;
+  rep->ecc_gvox_per_s = ecc_ms > 0 ? (double)n * it / (ecc_ms * 1e-3) / 1e9 : 0;
+  rep->last_points = m;
+  if (m > 0) {
+    CKR(cudaMemcpy(&rep->last_chi_first, ctx->chi.p, 8, cudaMemcpyDeviceToHost));
+    CKR(cudaMemcpy(&rep->last_chi_last, ctx->chi.as<int64_t>() + (m - 1), 8,
+                   cudaMemcpyDeviceToHost));
+  }
   return ECC_OK;
 }
 

@@ -46,6 +46,11 @@ cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys,
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
                             int64_t* changes, int64_t* chi, uint64_t* count, void* scratch,
                             cudaStream_t st);
+cudaError_t launch_uniform_noise(float* d, uint64_t n, uint64_t seed, int sms, cudaStream_t st);
+int gaussian_max_width();
+cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint64_t w1,
+                                 uint64_t w2, int axis, const double* d_weights, int width,
+                                 cudaStream_t st);
 cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
                         uint64_t base, int sms, cudaStream_t st);
 

@@ -23,6 +23,8 @@ int ecc_oracle_vcec_u8(const uint8_t*, uint64_t, uint64_t, uint64_t, int64_t*, i
 int ecc_oracle_vcec_u16(const uint16_t*, uint64_t, uint64_t, uint64_t, int64_t*, int64_t*);
 int64_t ecc_oracle_vcec_f32(const float*, uint64_t, uint64_t, uint64_t, float*, int64_t*);
 void ecc_oracle_fill_u8(uint8_t*, uint64_t, uint64_t, uint64_t);
+void ecc_oracle_uniform_noise(float*, uint64_t, uint64_t);
+int ecc_oracle_gaussian_smooth(const float*, float*, uint64_t, uint64_t, uint64_t, double, int);
 }
 
 using namespace ecc;
@@ -358,6 +360,25 @@ TEST_GPU("FileSource: raw f32 little / big endian, NaN and size errors (chunk.hp
   CHECK_THROWS_WITH(process_image(nan, plan), "NaN value at linear index 182");
   std::remove(le.c_str());
   std::remove(be.c_str());
+} END_TEST
+
+TEST_GPU("bench_run pipeline (pipeline.hpp:236-291) == oracle smoothing + ECC") {
+  const Dims d{20, 24, 28};
+  const auto rep = bench_run(d, 2, 1, 2.0, 13);
+  std::vector<float> x(d.voxel_count()), y(d.voxel_count());
+  ecc_oracle_uniform_noise(x.data(), x.size(), 1);
+  for (int it = 0; it < 2; ++it) {
+    CHECK(ecc_oracle_gaussian_smooth(x.data(), y.data(), d.w0, d.w1, d.w2, 2.0, 13) == 0);
+    x.swap(y);
+  }
+  Image<float> img{d, x};
+  const auto want = vcec_to_ecc(oracle_vcec(img));
+  CHECK(rep.iterations == 2 && rep.voxels == d.voxel_count());
+  CHECK(rep.last_points == want.size());
+  CHECK(rep.last_chi_first == want.chi.front() && rep.last_chi_last == want.chi.back());
+  CHECK(rep.to_string().find("ECC GVox/s:") != std::string::npos);
+  CHECK_THROWS_WITH(bench_run(d, 0), "at least one iteration");
+  CHECK_THROWS_WITH(bench_run(d, 1, 1, 2.0, 4), "odd and >= 1");
 } END_TEST
 
 // `test_api csv <file>`: file = u64 n, n float32 thresholds, n int64 chi;
