@@ -13,11 +13,13 @@
 // the same libm, capi.cu) and explicitly rounded __dmul_rn / __dadd_rn steps
 // the device produces the same floats.  Edge clamping as in the reference.
 //
-// Layout.  One thread per output voxel, a CTA row per image row (no 64-bit
-// index division); the taps of the contiguous axis hit L1, those of axes
-// 0 / 1 are coalesced rows that stay in L2 while a plane band is swept (13
-// planes x w1 x w2 x 4 B for the bench's width 13).  Double arithmetic: a
-// DMUL and a DADD per tap (no FMA: the reference rounds the product).
+// Layout.  Per smoothed axis the volume is (outer, L, inner).  Inputs are
+// staged once per CTA as doubles in shared memory, edge-clamped (the float
+// -> double conversion is exact and now happens once per input instead of
+// once per tap), then every thread runs several outputs: per tap one
+// conflict-free LDS.64, a DMUL and a DADD (no FMA: the reference rounds the
+// product).  inner == 1: row tiles of 1024 outputs; inner > 1: tiles of 32
+// coalesced inner positions x 64 outputs along the axis.
 #include <cstdint>
 
 #include "ecc_common.cuh"
@@ -39,41 +41,118 @@ __global__ void k_uniform(float* __restrict__ d, uint64_t n, uint64_t seed) {
     d[i] = (float)(splitmix64(seed + i * 0x9E3779B97F4A7C15ull) >> 40) * 0x1p-24f;
 }
 
-constexpr int MAXW = 1023;  // kernel taps held in shared memory
+constexpr int MAXW = 255;  // kernel taps (shared-memory tiles hold width - 1 halo lines)
 
-// One CTA row per image row (axes 0, 1 flattened: blockIdx.x), threads
-// along axis 2 (blockIdx.y tiles): no 64-bit division per voxel.
-__global__ void k_convolve_axis(const float* __restrict__ in, float* __restrict__ out,
-                                uint32_t w1, uint32_t w2, uint32_t axis_w, int axis,
-                                const double* __restrict__ w, int width) {
-  __shared__ double ws[MAXW];
-  for (int k = threadIdx.x; k < width; k += blockDim.x) ws[k] = w[k];
-  __syncthreads();
-  const uint32_t c = blockIdx.y * blockDim.x + threadIdx.x;
-  if (c >= w2) return;
-  const uint32_t r = blockIdx.x;
-  const uint32_t i0 = r / w1, i1 = r - i0 * w1;
-  const uint64_t i = (uint64_t)r * w2 + c;
-  const int64_t pos = axis == 0 ? i0 : (axis == 1 ? i1 : c);
-  const uint64_t s = axis == 0 ? (uint64_t)w1 * w2 : (axis == 1 ? w2 : 1);
-  const float* base = in + (i - (uint64_t)pos * s);
+// The volume seen as (outer, L, inner) around the smoothed axis (inner =
+// product of the later extents, the axis stride).  Inputs are staged once
+// as doubles in shared memory (edge-clamped), so a tap is one LDS.64, a
+// DMUL and a DADD; each thread produces several outputs.
+
+// inner == 1 (the contiguous axis): a CTA smooths 256 J consecutive outputs
+// of one line (J = 1, 2 or 4 by line length); thread t owns outputs
+// t + 256 j (conflict-free reads).
+constexpr int ROW_T = 256;
+
+template <int J>
+__global__ void __launch_bounds__(ROW_T)
+    k_smooth_rows(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
+                  uint32_t tiles, const double* __restrict__ w, int width) {
+  constexpr int ROW_J = J, ROW_OUT = ROW_T * J;
+  extern __shared__ double sh[];
+  double* ws = sh;                  // [width]
+  double* xs = sh + width;          // [J * ROW_T + width - 1]
   const int half = width / 2;
-  double acc = 0.0;
-  if (pos >= half && pos + half < (int64_t)axis_w) {
-    // interior (every voxel but the 2 x half nearest the ends): a running
-    // pointer, no clamping, no 64-bit index multiply per tap
-    const float* q = base + (uint64_t)(pos - half) * s;
-#pragma unroll 4
-    for (int k = 0; k < width; ++k, q += s)
-      acc = __dadd_rn(acc, __dmul_rn(ws[k], (double)__ldg(q)));
-  } else {
-    for (int k = -half; k <= half; ++k) {
-      int64_t qq = pos + k;
-      qq = qq < 0 ? 0 : (qq > (int64_t)axis_w - 1 ? (int64_t)axis_w - 1 : qq);
-      acc = __dadd_rn(acc, __dmul_rn(ws[k + half], (double)__ldg(base + (uint64_t)qq * s)));
+  const uint64_t line = blockIdx.x / tiles;
+  const int64_t p0 = (int64_t)(blockIdx.x - line * tiles) * ROW_OUT;
+  const float* src = in + line * L;
+  for (int k = threadIdx.x; k < width; k += ROW_T) ws[k] = w[k];
+  // staging: eight loads in flight per thread before any conversion
+  const int ne = J * ROW_T + width - 1;
+  for (int e0 = 0; e0 < ne; e0 += 8 * ROW_T) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * ROW_T + threadIdx.x;
+      int64_t q = p0 - half + e;
+      q = q < 0 ? 0 : (q > (int64_t)L - 1 ? (int64_t)L - 1 : q);
+      v[u] = e < ne ? __ldg(src + q) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * ROW_T + threadIdx.x;
+      if (e < ne) xs[e] = (double)v[u];
     }
   }
-  out[i] = __double2float_rn(acc);
+  __syncthreads();
+  double acc[ROW_J];
+#pragma unroll
+  for (int j = 0; j < ROW_J; ++j) acc[j] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    const double wk = ws[k];
+#pragma unroll
+    for (int j = 0; j < ROW_J; ++j)
+      acc[j] = __dadd_rn(acc[j], __dmul_rn(wk, xs[threadIdx.x + ROW_T * j + k]));
+  }
+  float* dst = out + line * L;
+#pragma unroll
+  for (int j = 0; j < ROW_J; ++j) {
+    const int64_t p = p0 + threadIdx.x + ROW_T * j;
+    if (p < (int64_t)L) dst[p] = __double2float_rn(acc[j]);
+  }
+}
+
+// inner > 1: a CTA smooths COL_W inner positions x COL_OUT outputs along the
+// axis; thread (c, g) owns column c, outputs g + COL_G j.
+constexpr int COL_W = 32, COL_G = 8, COL_J = 8, COL_OUT = COL_G * COL_J;
+
+__global__ void __launch_bounds__(COL_W * COL_G)
+    k_smooth_cols(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
+                  uint64_t inner, uint32_t ctiles, const double* __restrict__ w, int width) {
+  extern __shared__ double sh[];
+  double* ws = sh;                  // [width]
+  double* xs = sh + width;          // [(COL_OUT + width - 1) * COL_W]
+  const int half = width / 2;
+  const uint64_t outer = blockIdx.x / ctiles;
+  const uint64_t c0 = (uint64_t)(blockIdx.x - outer * ctiles) * COL_W;
+  const int64_t p0 = (int64_t)blockIdx.y * COL_OUT;
+  const float* src = in + outer * L * inner;
+  const int c = threadIdx.x & (COL_W - 1), g = threadIdx.x / COL_W;
+  const bool col_in = c0 + c < inner;
+  for (int k = threadIdx.x; k < width; k += COL_W * COL_G) ws[k] = w[k];
+  // staging: eight loads in flight per thread before any conversion
+  const int nr = COL_OUT + width - 1;
+  for (int r0 = g; r0 < nr; r0 += 8 * COL_G) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u * COL_G;
+      int64_t q = p0 - half + r;
+      q = q < 0 ? 0 : (q > (int64_t)L - 1 ? (int64_t)L - 1 : q);
+      v[u] = (col_in && r < nr) ? __ldg(src + (uint64_t)q * inner + c0 + c) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int r = r0 + u * COL_G;
+      if (r < nr) xs[r * COL_W + c] = (double)v[u];
+    }
+  }
+  __syncthreads();
+  double acc[COL_J];
+#pragma unroll
+  for (int j = 0; j < COL_J; ++j) acc[j] = 0.0;
+  for (int k = 0; k < width; ++k) {
+    const double wk = ws[k];
+#pragma unroll
+    for (int j = 0; j < COL_J; ++j)
+      acc[j] = __dadd_rn(acc[j], __dmul_rn(wk, xs[(g + COL_G * j + k) * COL_W + c]));
+  }
+  if (!col_in) return;
+  float* dst = out + outer * L * inner + c0 + c;
+#pragma unroll
+  for (int j = 0; j < COL_J; ++j) {
+    const int64_t p = p0 + g + COL_G * j;
+    if (p < (int64_t)L) dst[(uint64_t)p * inner] = __double2float_rn(acc[j]);
+  }
 }
 
 }  // namespace pipe
@@ -88,13 +167,40 @@ int gaussian_max_width() { return pipe::MAXW; }
 cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint64_t w1,
                                  uint64_t w2, int axis, const double* d_weights, int width,
                                  cudaStream_t st) {
-  const uint64_t rows = w0 * w1;
-  const uint64_t ext = axis == 0 ? w0 : (axis == 1 ? w1 : w2);
-  if (rows > 0x7FFFFFFFull || (w2 + 255) / 256 > 65535 || ext > 0xFFFFFFFFull)
-    return cudaErrorInvalidValue;
-  const dim3 grid((unsigned)rows, (unsigned)((w2 + 255) / 256));
-  pipe::k_convolve_axis<<<grid, 256, 0, st>>>(in, out, (uint32_t)w1, (uint32_t)w2, (uint32_t)ext,
-                                               axis, d_weights, width);
+  using namespace pipe;
+  const uint64_t ext[3] = {w0, w1, w2};
+  const uint64_t L = ext[axis];
+  uint64_t outer = 1, inner = 1;
+  for (int a = 0; a < axis; ++a) outer *= ext[a];
+  for (int a = axis + 1; a < 3; ++a) inner *= ext[a];
+  if (L > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  if (inner == 1) {
+    const int J = L <= 256 ? 1 : (L <= 512 ? 2 : 4);
+    const uint64_t tiles = (L + (uint64_t)ROW_T * J - 1) / ((uint64_t)ROW_T * J);
+    if (outer * tiles > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)(width + ROW_T * J + width - 1) * 8;
+    const unsigned grid = (unsigned)(outer * tiles);
+    auto go = [&](auto kern) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, ROW_T, smem, st>>>(in, out, (uint32_t)L, (uint32_t)tiles, d_weights, width);
+    };
+    if (J == 1)
+      go(k_smooth_rows<1>);
+    else if (J == 2)
+      go(k_smooth_rows<2>);
+    else
+      go(k_smooth_rows<4>);
+  } else {
+    const uint64_t ctiles = (inner + COL_W - 1) / COL_W;
+    const uint64_t ptiles = (L + COL_OUT - 1) / COL_OUT;
+    if (outer * ctiles > 0x7FFFFFFFull || ptiles > 65535) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)(width + (COL_OUT + width - 1) * COL_W) * 8;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_smooth_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_smooth_cols<<<dim3((unsigned)(outer * ctiles), (unsigned)ptiles), COL_W * COL_G, smem, st>>>(
+        in, out, (uint32_t)L, inner, (uint32_t)ctiles, d_weights, width);
+  }
   return cudaGetLastError();
 }
 
