@@ -487,15 +487,26 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
   CKI(ctx->asums.ensure(total_voxels * 8));
   CKR(launch_generic_changes(s, ECC_F32, ctx->ch8.as<int8_t>(), ctx->sms, st));
   const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
-  CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), ctx->flags.as<uint32_t>(),
-                        ctx->sms, st));
-  ctx->launches += 2;
+  // flags words 1, 2: min / max order key -> the bit range the sort must cover
+  uint32_t* mm = ctx->flags.as<uint32_t>() + 1;
+  {
+    const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    CKR(cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, st));
+  }
+  CKR(launch_key_range(owned, n64, ctx->flags.as<uint32_t>(), mm, ctx->sms, st));
+  CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), mm, ctx->sms, st));
+  ctx->launches += 3;
+  uint32_t range[2] = {0, 0};
+  CKR(cudaMemcpyAsync(range, mm, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  const uint32_t span = n64 ? range[1] - range[0] : 0;
+  const int bit0 = 0, bit1 = span ? 32 - __builtin_clz(span) : 1;
   uint32_t* out_keys = ctx->akeys.as<uint32_t>() + *n_acc;
   int64_t* out_sums = ctx->asums.as<int64_t>() + *n_acc;
   size_t t1 = 0, t2 = 0;
   CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, ctx->keys.as<uint32_t>(),
                                       ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
-                                      ctx->ch8b.as<int8_t>(), n, 0, 32, st));
+                                      ctx->ch8b.as<int8_t>(), n, bit0, bit1, st));
   auto vals = thrust::make_transform_iterator(ctx->ch8b.as<const int8_t>(), ToI64());
   CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(), out_keys, vals,
                                      out_sums, ctx->count.as<uint64_t>(), cub::Sum(), n, st));
@@ -503,7 +514,7 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
   t1 = ctx->tmp.cap;
   CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, ctx->keys.as<uint32_t>(),
                                       ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
-                                      ctx->ch8b.as<int8_t>(), n, 0, 32, st));
+                                      ctx->ch8b.as<int8_t>(), n, bit0, bit1, st));
   t2 = ctx->tmp.cap;
   CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(), out_keys, vals,
                                      out_sums, ctx->count.as<uint64_t>(), cub::Sum(), n, st));
@@ -511,6 +522,8 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
   uint64_t m = 0;
   CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
+  CKR(launch_add_key(out_keys, m, mm, ctx->sms, st));  // back to absolute order keys
+  ctx->launches += 1;
   *n_acc += m;
   return ECC_OK;
 }

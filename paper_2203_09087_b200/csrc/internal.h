@@ -39,8 +39,14 @@ cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
                                       cudaStream_t st);
 cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sms,
                                    cudaStream_t st);
-cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys,
-                              uint32_t* flags, int sms, cudaStream_t st);
+// sorted f32 path: key range (+ NaN flag), keys minus the minimum, and the
+// minimum added back to the reduced keys
+cudaError_t launch_key_range(const float* v, uint64_t n, uint32_t* flags, uint32_t* mm, int sms,
+                             cudaStream_t st);
+cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys, const uint32_t* mm,
+                              int sms, cudaStream_t st);
+cudaError_t launch_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm, int sms,
+                           cudaStream_t st);
 // K3; `scratch` (16 bytes per 1024 bins) enables the multi-CTA version for
 // large bin counts.
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,

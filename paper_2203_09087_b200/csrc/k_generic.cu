@@ -258,21 +258,65 @@ cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sm
 }
 
 // ---------------------------------------------------------------- order keys
-// Owned voxels -> order keys (value_index.hpp:95-99) for the sorted path,
-// plus a NaN check (ValueIndex<float>::build rejects NaN, value_index.hpp:29).
-__global__ void k_order_keys(const float* __restrict__ v, uint64_t n,
-                             uint32_t* __restrict__ keys, uint32_t* flags) {
+// Sorted path, pass 1: min / max order key of the owned voxels and the NaN
+// check (ValueIndex<float>::build rejects NaN, value_index.hpp:29).
+// mm[0] = min (start 0xFFFFFFFF), mm[1] = max (start 0).
+__global__ void k_key_range(const float* __restrict__ v, uint64_t n, uint32_t* flags,
+                            uint32_t* mm) {
+  uint32_t lo = 0xFFFFFFFFu, hi = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    const float x = v[i];
+    const float x = __ldg(v + i);
     if (x != x) atomicOr(flags, kFlagNaN);
-    keys[i] = float_order_key_bits(__float_as_uint(x));
+    const uint32_t k = float_order_key_bits(__float_as_uint(x));
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  lo = __reduce_min_sync(0xFFFFFFFFu, lo);
+  hi = __reduce_max_sync(0xFFFFFFFFu, hi);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(mm, lo);
+    atomicMax(mm + 1, hi);
   }
 }
 
-cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys,
-                              uint32_t* flags, int sms, cudaStream_t st) {
-  k_order_keys<<<sms * 8, 256, 0, st>>>(v, n, keys, flags);
+// Pass 2: order keys (value_index.hpp:95-99) minus the minimum -- still
+// order-preserving, and only the low bits of (max - min) vary, so the radix
+// sort covers fewer bits (the reference skips trivial passes,
+// value_index.hpp:125-131, for the same reason).
+__global__ void k_order_keys(const float* __restrict__ v, uint64_t n,
+                             uint32_t* __restrict__ keys, const uint32_t* mm) {
+  const uint32_t lo = mm[0];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] = float_order_key_bits(__float_as_uint(v[i])) - lo;
+}
+
+__global__ void k_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm) {
+  const uint32_t lo = mm[0];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    keys[i] += lo;
+}
+
+cudaError_t launch_key_range(const float* v, uint64_t n, uint32_t* flags, uint32_t* mm, int sms,
+                             cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_key_range<<<sms * 8, 256, 0, st>>>(v, n, flags, mm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_order_keys(const float* v, uint64_t n, uint32_t* keys, const uint32_t* mm,
+                              int sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_order_keys<<<sms * 8, 256, 0, st>>>(v, n, keys, mm);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm, int sms,
+                           cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_add_key<<<sms * 4, 256, 0, st>>>(keys, n, mm);
   return cudaGetLastError();
 }
 
