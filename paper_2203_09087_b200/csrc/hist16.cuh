@@ -22,25 +22,29 @@ namespace hist16 {
 constexpr uint32_t BIAS = 0x80008000u;
 
 struct Upd {
-  uint32_t key, add, old, mult;
+  uint32_t key, add, old;
 };
 
-// add the signed change chu (two's complement; 0 = no-op) to bin `key`
+// add the signed change chu (two's complement; 0 = no-op) to bin `key`.
+// chu << (16 * (key & 1)) is one wrap-mode funnel shift by key << 4 (the
+// shift amount is taken mod 32).
 __device__ __forceinline__ void issue(uint32_t hbase, uint32_t key, uint32_t chu, Upd& u) {
   u.key = key;
-  u.mult = 1u + 65535u * (key & 1u);  // 1 or 65536: low or high half
-  u.add = chu * u.mult;
+  u.add = __funnelshift_l(0u, chu, key << 4);
   // unconditional: a zero add is cheaper than the branch ptxas makes of a
   // predicated atomic with a return value (ISETP + BSSY + BRA + BSYNC)
   asm volatile("atom.shared.add.u32 %0, [%1], %2;"
                : "=r"(u.old)
-               : "r"(hbase + ((key << 1) & ~3u)), "r"(u.add)
+               : "r"(hbase + (key >> 1) * 4u), "r"(u.add)
                : "memory");
 }
 
+// Band change of the updated half.  Only that half can differ between the
+// old and new word (the band keeps the low half from carrying into the high
+// one), so one constant mask covers both halves.
 __device__ __forceinline__ uint32_t crossed(const Upd& u) {
   const uint32_t d = u.old ^ (u.old + u.add);
-  return (d ^ (d << 1)) & (0x8000u * u.mult);
+  return (d ^ (d << 1)) & 0x80008000u;
 }
 
 // the rare fix: predicated shared add of -after, and `spill(key, after)`
@@ -49,7 +53,7 @@ __device__ __forceinline__ void fix(uint32_t hbase, const Upd& u, uint32_t cross
   if (cross) {
     const uint32_t sh = (u.key & 1u) << 4;
     const int after = (int)(((u.old + u.add) >> sh) & 0xFFFFu) - 32768;
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hbase + ((u.key << 1) & ~3u)),
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hbase + (u.key >> 1) * 4u),
                  "r"((uint32_t)(-after) << sh)
                  : "memory");
     spill(u.key, after);
@@ -60,8 +64,8 @@ __device__ __forceinline__ void fix(uint32_t hbase, const Upd& u, uint32_t cross
 // (OR-ing 0 is a no-op); cheaper than testing the bit first, which ptxas
 // turns into a load, a compare and a branch per pixel.
 __device__ __forceinline__ void mark(uint32_t pbase, uint32_t key, uint32_t own) {
-  const uint32_t pa = pbase + ((key >> 3) & ~3u);
-  const uint32_t bit = own << (key & 31);
+  const uint32_t pa = pbase + (key >> 5) * 4u;
+  const uint32_t bit = __funnelshift_l(0u, own, key);  // own << (key & 31)
   asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(pa), "r"(bit) : "memory");
 }
 
