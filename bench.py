@@ -13,9 +13,11 @@ N grows ("scaling": "weak").
                on the compute stream, max over ranks, L2 flushed (256 MiB
                write) between timed steps.
 * e2e       -- the same metric through the public C ABI with a pinned HOST
-               buffer (ecc_curve for N = 1; per-rank H2D + slab + all-reduce +
-               finalize + D2H for N > 1), host<->device copies inside the
-               timed region.
+               buffer (ecc_curve for N = 1: the H2D is split into plane chunks
+               on a copy stream and each chunk's kernel runs as soon as it
+               and its halo plane have landed; per-rank H2D + slab +
+               all-reduce + finalize + D2H for N > 1), host<->device copies
+               inside the timed region.
 * roofline  -- the dominant kernel (k_u8_3d: K1+K2, with K3 fused at N = 1):
                algorithmic bytes (1 B/voxel read) / its CUDA-event time vs
                MEASURED_PEAKS.json hbm_gbs.

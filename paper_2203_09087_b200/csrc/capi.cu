@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -144,6 +145,7 @@ struct ecc_ctx {
   DevBuf sm_tmp[2], sm_w;     // gaussian_smooth: axis temporaries and the taps
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
+  cudaEvent_t ov_ev[17] = {};  // overlapped host-input path: start + one per chunk copy
 };
 
 namespace {
@@ -762,6 +764,8 @@ int ecc_ctx_create(int device, ecc_ctx** out) {
 void ecc_ctx_destroy(ecc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  for (cudaEvent_t& e : ctx->ov_ev)
+    if (e) cudaEventDestroy(e);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->copy);
   for (DevBuf* b : {&ctx->input, &ctx->hist, &ctx->bins, &ctx->changes, &ctx->chi,
@@ -872,6 +876,57 @@ int ecc_finalize(ecc_ctx* ctx, const int64_t* d_hist, uint64_t nbins, uint32_t* 
   return ECC_OK;
 }
 
+// A large 3D u8 image in host memory: the H2D copy is split into plane
+// chunks on the copy stream and each chunk's K1+K2 runs on the compute
+// stream as soon as it and the next chunk (its halo plane) have landed, so
+// only the last chunk's kernel and K3 remain after the copy; the image is
+// still one resident volume (one TMA descriptor), chunks differ only in
+// their owned planes.  Returns handled = false when the shape does not fit.
+int overlapped_u8(ecc_ctx* ctx, const void* host, ecc_dims dims, cudaStream_t st, BinResult* r,
+                  bool* handled) {
+  *handled = false;
+  const uint64_t plane = dims.w1 * dims.w2, bytes = dims.w0 * plane;
+  if (dims.w2 <= 1 || bytes < (32ull << 20) || dims.w0 < 8) return ECC_OK;
+  static const char* env = std::getenv("ECC_B200_OVERLAP_CHUNKS");  // tuning / A-B hook
+  const int env_nc = env ? std::atoi(env) : -1;
+  if (env_nc == 0) return ECC_OK;
+  CKI(ctx->input.ensure(bytes));
+  const Slab s = make_slab(ctx->input.p, dims, 0, dims.w0, 0, dims.w0);
+  if (!u8_3d_supported(s)) return ECC_OK;
+  // 16 MB chunks, at most 8 (measured on C2, 128 MB: 1 chunk 3.31 ms, 2: 2.62,
+  // 4: 2.57, 8: 2.56, 16: 3.40 -- many small copies lose DMA efficiency)
+  int nc = (int)std::min<uint64_t>(8, std::min<uint64_t>(dims.w0 / 4, bytes >> 24));
+  if (env_nc > 0) nc = (int)std::min<uint64_t>(std::min(env_nc, 16), dims.w0);
+  nc = std::max(nc, 1);
+  for (int k = 0; k <= nc; ++k)
+    if (!ctx->ov_ev[k]) CKR(cudaEventCreateWithFlags(&ctx->ov_ev[k], cudaEventDisableTiming));
+  CKI(ctx->hist.ensure(512 * 8));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 512 * 8, st));
+  // copies start after everything already queued on the compute stream
+  CKR(cudaEventRecord(ctx->ov_ev[nc], st));
+  CKR(cudaStreamWaitEvent(ctx->copy, ctx->ov_ev[nc], 0));
+  std::vector<uint64_t> b(nc + 1);
+  for (int k = 0; k <= nc; ++k) b[k] = dims.w0 * k / nc;
+  for (int k = 0; k < nc; ++k) {
+    CKR(cudaMemcpyAsync(ctx->input.as<uint8_t>() + b[k] * plane,
+                        static_cast<const uint8_t*>(host) + b[k] * plane, (b[k + 1] - b[k]) * plane,
+                        cudaMemcpyHostToDevice, ctx->copy));
+    CKR(cudaEventRecord(ctx->ov_ev[k], ctx->copy));
+  }
+  for (int k = 0; k < nc; ++k) {
+    CKR(cudaStreamWaitEvent(st, ctx->ov_ev[k], 0));
+    if (k + 1 < nc) CKR(cudaStreamWaitEvent(st, ctx->ov_ev[k + 1], 0));
+    Slab sk = s;
+    sk.own0 = (int64_t)b[k];
+    sk.own1 = (int64_t)b[k + 1];
+    CKR(launch_u8_3d(sk, ctx->hist.as<int64_t>(), nullptr, ctx->sms, st));
+    ctx->launches += 1;
+  }
+  CKI(finalize_to_host(ctx, 256, st, r));
+  *handled = true;
+  return ECC_OK;
+}
+
 static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
                          ecc_dims dims, const ecc_binmap* bm, void* values_out,
                          int64_t* series_out, uint64_t cap, uint64_t* n_out, bool want_chi) {
@@ -881,12 +936,17 @@ static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dt
   if (!data || !values_out || !series_out || !n_out) return fail(ECC_EINVAL, "null pointer");
   cudaStream_t st = ctx->stream;
   const uint64_t bytes = dims.w0 * dims.w1 * dims.w2 * esize(dtype);
-  const void* d_data = nullptr;
-  CKI(stage_input(ctx, data, where, bytes, st, &d_data));
   BinResult r;
   bool sorted = false;
   AffineMap am{};
-  CKI(run_volume(ctx, d_data, dtype, dims, bm, st, &r, &sorted, &am));
+  bool done = false;
+  if (where == 0 && dtype == ECC_U8 && (!bm || bm->kind == ECC_BIN_IDENTITY))
+    CKI(overlapped_u8(ctx, data, dims, st, &r, &done));
+  if (!done) {
+    const void* d_data = nullptr;
+    CKI(stage_input(ctx, data, where, bytes, st, &d_data));
+    CKI(run_volume(ctx, d_data, dtype, dims, bm, st, &r, &sorted, &am));
+  }
   const size_t m = r.changes.size();
   *n_out = m;
   if (m > cap) return fail(ECC_EINVAL, "output capacity " + std::to_string(cap) +

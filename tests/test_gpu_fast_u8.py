@@ -131,3 +131,15 @@ def test_odd_row_widths_take_the_padded_fast_path(ctx, shape):
     got = ctx.vcec(dev)
     v, c = oracle.vcec(img)
     assert np.array_equal(got.changes, c)
+
+
+@pytest.mark.parametrize("shape", [(256, 512, 512), (130, 512, 512), (67, 700, 768)])
+def test_overlapped_host_input(ctx, shape):
+    """Large host u8 volumes take the overlapped path of ecc_vcec / ecc_curve
+    (chunked H2D on the copy stream, each chunk's kernel as soon as it and
+    its halo plane have landed); the curve equals the oracle's."""
+    rng = np.random.default_rng(sum(shape))
+    img = rng.integers(0, 256, shape, dtype=np.uint8)
+    _check(ctx, img)
+    c = ctx.curve(img)
+    assert int(c.chi[-1]) == 1
