@@ -2,12 +2,28 @@
 // the C ABI (capi.cu).  Not installed; the public boundary is
 // include/ecc_b200.h.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "ecc_common.cuh"
 
 namespace eccb {
+
+// Opt kernel FN in to `bytes` of dynamic shared memory, once per device (the
+// attribute is per device; a process may drive several GPUs, one context
+// each).
+template <auto FN>
+inline void smem_optin(int bytes) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_relaxed) & bit)) {
+    cudaFuncSetAttribute(FN, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit);
+  }
+}
 
 // Workspace of the fused single-launch curve (k_u8_3d.cu): `ticket` and the
 // 512-entry int64 histogram must be zero before the launch and are zero

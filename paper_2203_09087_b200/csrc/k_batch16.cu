@@ -298,11 +298,7 @@ cudaError_t launch_batch16(const uint16_t* data, uint64_t count, int h, int w, i
   int L = 1;
   while (L < (w + 31) / 32) L <<= 1;
   const size_t smem = (size_t)(HWORDS + 2 * PWORDS) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_batch16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  smem_optin<k_batch16>((int)smem);
   k_batch16<<<(unsigned)count, NT, smem, st>>>(data, h, w, L, chi, presence, spill_scratch);
   return cudaGetLastError();
 }

@@ -256,11 +256,7 @@ cudaError_t launch_u16_2d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   const long long units = (g.P + band - 1) / band * g.nstrips;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_u16_2d, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
+  smem_optin<k_u16_2d>(SMEM_BYTES);
   const long long grid = std::min<long long>((units + NW - 1) / NW, sms);
   k_u16_2d<<<(unsigned)grid, NT, SMEM_BYTES, st>>>(g, ghist);
   return cudaGetLastError();

@@ -546,11 +546,7 @@ cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   g.Gz = (g.W2 + 29) / 30;
   g.ncols = g.Gy * g.Gz;
   g.nbins = nbins;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_u16_3d, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    attr = true;
-  }
+  smem_optin<k_u16_3d>(SMEM_BYTES);
   const long long cap_warps = (long long)sms * NW;
   const long long nseg = best_segments(g.ncols, g.P, cap_warps);
   g.seglen = (int)((g.P + nseg - 1) / nseg);

@@ -473,14 +473,16 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.ncols = g.Gy * g.Gz;
   g.chg = chg;
   g.four = 4;
-  static int per_sm = -1;
+  smem_optin<k_u8_3d<false>>(SMEM_BYTES);
+  smem_optin<k_u8_3d<true>>(SMEM_BYTES);
+  static int per_sm = -1;  // same on every B200
   if (per_sm < 0) {
-    cudaFuncSetAttribute(k_u8_3d<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    cudaFuncSetAttribute(k_u8_3d<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_u8_3d<false>, NW * 32, SMEM_BYTES) !=
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_u8_3d<false>, NW * 32, SMEM_BYTES) !=
             cudaSuccess ||
-        per_sm < 1)
-      per_sm = 1;
+        v < 1)
+      v = 1;
+    per_sm = v;
   }
   const long long cap_warps = (long long)sms * per_sm * NW;
   // Segments along axis 0: one wave of (segment, column) units when the
