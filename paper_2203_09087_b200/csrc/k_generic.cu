@@ -107,20 +107,35 @@ __global__ void k_generic3(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
   const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
   const int64_t i1 = min(i0 + seg, s.own1);
   if (j < s.w1 && k < s.w2 && i0 < i1) {
+    // per-thread: which in-plane neighbours exist (mask bit 3b + c) and the
+    // element offset of the centre of plane i (+ i * plane); no per-load
+    // 64-bit index products or 6-way bounds tests
+    uint32_t inb = 0;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        if (j - 1 + b >= 0 && j - 1 + b < s.w1 && k - 1 + c >= 0 && k - 1 + c < s.w2)
+          inb |= 1u << (3 * b + c);
+    const T* base = static_cast<const T*>(s.base);
+    const int64_t plane = s.w1 * s.w2, row = s.w2;
+    const T* ctr = base + (j * s.w2 + k) - s.plane0 * plane;
+    auto load_plane = [&](int64_t ii, uint32_t (&out)[3][3]) {
+      const uint32_t m = (ii >= 0 && ii < s.w0) ? inb : 0u;
+      const T* pc = ctr + ii * plane;
+#pragma unroll
+      for (int b = 0; b < 3; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          out[b][c] = ((m >> (3 * b + c)) & 1u)
+                          ? KeyTraits<T>::key(__ldg(pc + (b - 1) * row + (c - 1)))
+                          : KeyTraits<T>::kSentinel;
+    };
     uint32_t w[3][3][3];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          w[a][b][c] = ldkey<T>(s, i0 - 1 + a, j - 1 + b, k - 1 + c);
+    load_plane(i0 - 1, w[0]);
+    load_plane(i0, w[1]);
     for (int64_t i = i0; i < i1; ++i) {
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          w[2][b][c] = ldkey<T>(s, i + 1, j - 1 + b, k - 1 + c);
+      load_plane(i + 1, w[2]);
       const int ch = change3(w);
       if constexpr (HIST) {
         const T v = ldval<T>(s, i, j, k);
