@@ -26,7 +26,10 @@
 namespace eccb {
 namespace b16 {
 
-constexpr int NW = 16;  // warps per CTA
+#ifndef ECC_B16_NW
+#define ECC_B16_NW 16
+#endif
+constexpr int NW = ECC_B16_NW;  // warps per CTA
 constexpr int NT = NW * 32;
 constexpr int HWORDS = 32768, PWORDS = 2048;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -226,11 +229,12 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
   __syncthreads();
-  // epilogue, conflict-free: warp w owns bins [w * 4096, (w + 1) * 4096) in
-  // 32 chunks of 128; lane l holds 4 consecutive bins of a chunk (one 8-byte
+  // epilogue, conflict-free: warp w owns a contiguous run of 128-bin chunks
+  // (32 for 16 warps); lane l holds 4 consecutive bins of a chunk (one 8-byte
   // shared load, the chunk's spill bits one broadcast word).  Pass 1 sums the
   // warp's bins, pass 2 scans chunk by chunk and writes chi coalesced.
-  constexpr uint32_t PER_WARP = 65536 / NW;
+  // warp w owns the 128-bin chunks [c0, c1) (contiguous, in order)
+  const uint32_t c0 = (uint32_t)warp * 512u / NW, c1 = (uint32_t)(warp + 1) * 512u / NW;
   int32_t* row = chi + (size_t)blockIdx.x * 65536;
   auto sums4 = [&](uint32_t b, int (&x)[4]) {  // b % 4 == 0
     const uint2 w2 = *reinterpret_cast<const uint2*>(hw + (b >> 1));
@@ -246,9 +250,9 @@ __global__ void __launch_bounds__(NT, 1)
     }
   };
   __shared__ int32_t wsum[NW];
-  const uint32_t wb = (uint32_t)warp * PER_WARP + 4u * lane;
+  const uint32_t wb = 4u * lane;
   int32_t part = 0;
-  for (uint32_t i = 0; i < PER_WARP; i += 128) {
+  for (uint32_t i = c0 * 128u; i < c1 * 128u; i += 128) {
     int x[4];
     sums4(wb + i, x);
     part += x[0] + x[1] + x[2] + x[3];
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   int32_t carry = 0;
   for (int j = 0; j < warp; ++j) carry += wsum[j];
-  for (uint32_t i = 0; i < PER_WARP; i += 128) {
+  for (uint32_t i = c0 * 128u; i < c1 * 128u; i += 128) {
     int x[4];
     sums4(wb + i, x);
     x[1] += x[0];
