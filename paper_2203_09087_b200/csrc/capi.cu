@@ -907,22 +907,30 @@ int overlapped_u8(ecc_ctx* ctx, const void* host, ecc_dims dims, cudaStream_t st
   CKR(cudaStreamWaitEvent(ctx->copy, ctx->ov_ev[nc], 0));
   std::vector<uint64_t> b(nc + 1);
   for (int k = 0; k <= nc; ++k) b[k] = dims.w0 * k / nc;
-  for (int k = 0; k < nc; ++k) {
-    CKR(cudaMemcpyAsync(ctx->input.as<uint8_t>() + b[k] * plane,
-                        static_cast<const uint8_t*>(host) + b[k] * plane, (b[k + 1] - b[k]) * plane,
-                        cudaMemcpyHostToDevice, ctx->copy));
-    CKR(cudaEventRecord(ctx->ov_ev[k], ctx->copy));
+  int rc = ECC_OK;
+  for (int k = 0; k < nc && rc == ECC_OK; ++k) {
+    cudaError_t e = cudaMemcpyAsync(ctx->input.as<uint8_t>() + b[k] * plane,
+                                    static_cast<const uint8_t*>(host) + b[k] * plane,
+                                    (b[k + 1] - b[k]) * plane, cudaMemcpyHostToDevice, ctx->copy);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ov_ev[k], ctx->copy);
+    if (e != cudaSuccess) rc = fail(ECC_ECUDA, cudaGetErrorString(e));
   }
-  for (int k = 0; k < nc; ++k) {
-    CKR(cudaStreamWaitEvent(st, ctx->ov_ev[k], 0));
-    if (k + 1 < nc) CKR(cudaStreamWaitEvent(st, ctx->ov_ev[k + 1], 0));
+  for (int k = 0; k < nc && rc == ECC_OK; ++k) {
+    cudaError_t e = cudaStreamWaitEvent(st, ctx->ov_ev[k], 0);
+    if (e == cudaSuccess && k + 1 < nc) e = cudaStreamWaitEvent(st, ctx->ov_ev[k + 1], 0);
     Slab sk = s;
     sk.own0 = (int64_t)b[k];
     sk.own1 = (int64_t)b[k + 1];
-    CKR(launch_u8_3d(sk, ctx->hist.as<int64_t>(), nullptr, ctx->sms, st));
+    if (e == cudaSuccess) e = launch_u8_3d(sk, ctx->hist.as<int64_t>(), nullptr, ctx->sms, st);
+    if (e != cudaSuccess) rc = fail(ECC_ECUDA, cudaGetErrorString(e));
     ctx->launches += 1;
   }
-  CKI(finalize_to_host(ctx, 256, st, r));
+  if (rc == ECC_OK) rc = finalize_to_host(ctx, 256, st, r);
+  if (rc != ECC_OK) {
+    // no copy into ctx->input may outlive the call
+    cudaStreamSynchronize(ctx->copy);
+    return rc;
+  }
   *handled = true;
   return ECC_OK;
 }
