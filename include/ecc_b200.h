@@ -205,6 +205,22 @@ ECC_API int ecc_process_file(ecc_ctx* ctx, const char* path, ecc_dtype dtype, ec
                      const ecc_binmap* bm, ecc_chunk_timing* timings, void* values_out,
                      int64_t* changes_out, uint64_t cap, uint64_t* n_out);
 
+/* ------------------------------------------------------------ sharded streaming
+ * a rank's share of a host image (C5 on several GPUs).
+ * Accumulates the owned planes [bounds[0], bounds[nchunks]) into the device
+ * histogram d_hist (int64[2 * nbins] as in ecc_accumulate_slab; NOT zeroed
+ * here) chunk by chunk with the pipelined DMA of ecc_process_host: chunk k
+ * owns [bounds[k], bounds[k+1]) and its halo planes come from the same host
+ * buffer, which holds image planes [plane0, plane0 + nplanes).  The bounds
+ * must increase within [0, w0] but need not start at 0 or end at w0 (each
+ * rank passes its own range); combine ranks with one all-reduce of d_hist and
+ * ecc_finalize.  Synchronous.  Replaces, per rank, the reference's
+ * process_image over a chunk plan (streaming.hpp:181-329). */
+ECC_API int ecc_accumulate_host(ecc_ctx* ctx, const void* host_planes, uint64_t plane0,
+                                uint64_t nplanes, ecc_dtype dtype, ecc_dims image,
+                                const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
+                                int64_t* d_hist);
+
 /* ------------------------------------------------------------ batched 2D
  * New entry point (the reference has none): `count` images of
  * h x w (axis 0 = h), stored back to back.  For each image b, writes the

@@ -111,6 +111,9 @@ def lib() -> C.CDLL:
             L.ecc_process_host.argtypes = [_vp, _vp, C.c_int, _Dims, C.POINTER(_u64), C.c_size_t,
                                            C.POINTER(_BinMap), C.POINTER(_Timing), _vp, _vp, _u64,
                                            C.POINTER(_u64)]
+            L.ecc_accumulate_host.argtypes = [_vp, _vp, _u64, _u64, C.c_int, _Dims,
+                                              C.POINTER(_u64), C.c_size_t, C.POINTER(_BinMap), _vp]
+            L.ecc_accumulate_host.restype = C.c_int
             L.ecc_process_file.argtypes = [_vp, C.c_char_p, C.c_int, _Dims, C.c_int, C.POINTER(_u64),
                                            C.c_size_t, C.POINTER(_BinMap), C.POINTER(_Timing), _vp,
                                            _vp, _u64, C.POINTER(_u64)]
@@ -590,6 +593,22 @@ class Context:
         return GlobalVcec(vals[:m].copy(), ch[:m].copy())
 
     # -------------------------------------------------------------- lower level
+    def accumulate_host(self, planes, plane0: int, dims: Dims, bounds, hist, binmap=None):
+        """ecc_accumulate_host: a rank's owned planes [bounds[0], bounds[-1])
+        of a host image whose planes [plane0, plane0 + len(planes)) are in
+        `planes` (numpy or a CPU torch tensor; pinned memory streams at full
+        PCIe speed), accumulated chunk by chunk into the device int64
+        histogram `hist` (torch, 2*nbins, not zeroed here)."""
+        if not isinstance(planes, np.ndarray):
+            planes = planes.numpy()
+        planes = np.ascontiguousarray(planes)
+        dt = _DT[planes.dtype]
+        b = (_u64 * len(bounds))(*[int(x) for x in bounds])
+        bm = _binmap(dt, binmap)
+        _check(lib().ecc_accumulate_host(self._p, planes.ctypes.data, plane0, planes.shape[0], dt,
+                                         _Dims(dims.w0, dims.w1, dims.w2), b, len(bounds) - 1,
+                                         C.byref(bm), hist.data_ptr()))
+
     def accumulate_slab(self, planes, dims: Dims, plane0: int, own0: int, own1: int,
                         hist, binmap=None, stream: int = 0):
         """K1+K2 into a device int64 histogram tensor of 2*nbins (torch)."""

@@ -1216,6 +1216,104 @@ int ecc_process_file(ecc_ctx* ctx, const char* path, ecc_dtype dtype, ecc_dims d
   return rc;
 }
 
+}  // extern "C"
+
+namespace {
+
+// The pipelined host-DMA loop shared by ecc_process_host and
+// ecc_accumulate_host: chunk k's planes + halo are copied (copy stream) from
+// the caller's host buffer -- which holds image planes [plane0, plane0 +
+// nheld) -- into one of three device slabs while earlier chunks' kernels run
+// (compute stream), accumulating into `hist`.  Synchronous.
+int host_pipeline(ecc_ctx* ctx, const void* host, uint64_t plane0, uint64_t nheld,
+                  ecc_dtype dtype, ecc_dims dims, const uint64_t* bounds, size_t nchunks,
+                  bool affine, const AffineMap& am, uint64_t nbins, int64_t* hist,
+                  ecc_chunk_timing* timings) {
+  const auto t0 = std::chrono::steady_clock::now();
+  auto since = [&] {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  };
+  const uint64_t row_bytes = dims.w1 * dims.w2 * esize(dtype);
+  uint64_t max_rows = 0;
+  for (size_t k = 0; k < nchunks; ++k) {
+    const uint64_t r0 = bounds[k] == 0 ? 0 : bounds[k] - 1;
+    const uint64_t r1 = std::min<uint64_t>(bounds[k + 1] + 1, dims.w0);
+    if (r0 < plane0 || r1 > plane0 + nheld)
+      return fail(ECC_EINVAL, "chunk " + std::to_string(k) + " needs planes [" +
+                                  std::to_string(r0) + ", " + std::to_string(r1) +
+                                  ") but the host buffer holds [" + std::to_string(plane0) +
+                                  ", " + std::to_string(plane0 + nheld) + ")");
+    max_rows = std::max<uint64_t>(max_rows, r1 - r0);
+  }
+  constexpr int NB = 3;  // device slab buffers in flight
+  for (int b = 0; b < NB; ++b) CKI(ctx->slab[b].ensure(max_rows * row_bytes));
+  cudaStream_t st = ctx->stream, cp = ctx->copy;
+  std::vector<cudaEvent_t> ev(4 * nchunks + 1);
+  for (auto& e : ev) CKR(cudaEventCreate(&e));
+  auto evh0 = [&](size_t k) { return ev[4 * k + 0]; };  // H2D begin
+  auto evh1 = [&](size_t k) { return ev[4 * k + 1]; };  // H2D end
+  auto evk0 = [&](size_t k) { return ev[4 * k + 2]; };  // kernel begin
+  auto evk1 = [&](size_t k) { return ev[4 * k + 3]; };  // kernel end
+  cudaEvent_t start = ev[4 * nchunks];
+  // copies start after everything already queued on the compute stream
+  CKR(cudaEventRecord(start, st));
+  CKR(cudaStreamWaitEvent(cp, start, 0));
+  const double t_start = since();
+  int rc = ECC_OK;
+  for (size_t k = 0; k < nchunks && rc == ECC_OK; ++k) {
+    const int b = (int)(k % NB);
+    const uint64_t own0 = bounds[k], own1 = bounds[k + 1];
+    const uint64_t r0 = own0 == 0 ? 0 : own0 - 1;
+    const uint64_t r1 = std::min<uint64_t>(own1 + 1, dims.w0);
+    cudaError_t e = cudaSuccess;
+    if (k >= (size_t)NB) e = cudaStreamWaitEvent(cp, evk1(k - NB), 0);  // buffer reuse
+    if (e == cudaSuccess) e = cudaEventRecord(evh0(k), cp);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ctx->slab[b].p,
+                          static_cast<const uint8_t*>(host) + (r0 - plane0) * row_bytes,
+                          (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, cp);
+    if (e == cudaSuccess) e = cudaEventRecord(evh1(k), cp);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, evh1(k), 0);
+    if (e == cudaSuccess) e = cudaEventRecord(evk0(k), st);
+    if (e != cudaSuccess) {
+      rc = fail(ECC_ECUDA, cudaGetErrorString(e));
+      break;
+    }
+    const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
+    rc = accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, hist, st);
+    if (rc == ECC_OK && cudaEventRecord(evk1(k), st) != cudaSuccess)
+      rc = fail(ECC_ECUDA, "event record failed");
+  }
+  const cudaError_t e1 = cudaStreamSynchronize(cp);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  if (rc == ECC_OK && (e1 != cudaSuccess || e2 != cudaSuccess))
+    rc = fail(ECC_ECUDA, cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  if (rc == ECC_OK && timings) {
+    for (size_t k = 0; k < nchunks; ++k) {
+      float a = 0, b = 0, c = 0, d = 0;
+      cudaEventElapsedTime(&a, start, evh0(k));
+      cudaEventElapsedTime(&b, start, evh1(k));
+      cudaEventElapsedTime(&c, start, evk0(k));
+      cudaEventElapsedTime(&d, start, evk1(k));
+      ecc_chunk_timing& t = timings[k];
+      t.begin = bounds[k];
+      t.end = bounds[k + 1];
+      t.ingest_begin = t_start + a * 1e-3;
+      t.ingest_end = t_start + b * 1e-3;
+      t.index_begin = t.index_end = t.ingest_end;
+      t.kernel_begin = t_start + c * 1e-3;
+      t.kernel_end = t_start + d * 1e-3;
+      t.merge_begin = t.merge_end = t.kernel_end;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
 int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims dims,
                      const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
                      ecc_chunk_timing* timings, void* values_out, int64_t* changes_out,
@@ -1233,79 +1331,46 @@ int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims d
     return fail(ECC_EINVAL, "the sorted bin map streams through ecc_process_stream");
   // pinned (page-locked or registered) memory is copied by DMA straight from
   // the caller's buffer; pageable memory makes each copy synchronous
-  const auto t0 = std::chrono::steady_clock::now();
-  auto since = [&] {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  };
-  const uint64_t row_bytes = dims.w1 * dims.w2 * esize(dtype);
-  uint64_t max_rows = 0;
-  for (size_t k = 0; k < nchunks; ++k)
-    max_rows = std::max<uint64_t>(max_rows, bounds[k + 1] - bounds[k] + 2);
-  max_rows = std::min<uint64_t>(max_rows, dims.w0);
-  constexpr int NB = 3;  // device slab buffers in flight
-  for (int b = 0; b < NB; ++b) CKI(ctx->slab[b].ensure(max_rows * row_bytes));
   CKI(ctx->flags.ensure(4));
   CKI(ctx->hist.ensure(2 * nbins * 8));
-  cudaStream_t st = ctx->stream, cp = ctx->copy;
+  cudaStream_t st = ctx->stream;
   CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
   CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
-  std::vector<cudaEvent_t> ev(4 * nchunks + 1);
-  for (auto& e : ev) CKR(cudaEventCreate(&e));
-  auto evh0 = [&](size_t k) { return ev[4 * k + 0]; };  // H2D begin
-  auto evh1 = [&](size_t k) { return ev[4 * k + 1]; };  // H2D end
-  auto evk0 = [&](size_t k) { return ev[4 * k + 2]; };  // kernel begin
-  auto evk1 = [&](size_t k) { return ev[4 * k + 3]; };  // kernel end
-  cudaEvent_t start = ev[4 * nchunks];
-  CKR(cudaEventRecord(start, cp));
-  const double t_start = since();
-  int rc = ECC_OK;
-  for (size_t k = 0; k < nchunks && rc == ECC_OK; ++k) {
-    const int b = (int)(k % NB);
-    const uint64_t own0 = bounds[k], own1 = bounds[k + 1];
-    const uint64_t r0 = own0 == 0 ? 0 : own0 - 1;
-    const uint64_t r1 = std::min<uint64_t>(own1 + 1, dims.w0);
-    if (k >= (size_t)NB) CKR(cudaStreamWaitEvent(cp, evk1(k - NB), 0));  // buffer reuse
-    CKR(cudaEventRecord(evh0(k), cp));
-    CKR(cudaMemcpyAsync(ctx->slab[b].p, static_cast<const uint8_t*>(host) + r0 * row_bytes,
-                        (r1 - r0) * row_bytes, cudaMemcpyHostToDevice, cp));
-    CKR(cudaEventRecord(evh1(k), cp));
-    CKR(cudaStreamWaitEvent(st, evh1(k), 0));
-    CKR(cudaEventRecord(evk0(k), st));
-    const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
-    rc = accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st);
-    CKR(cudaEventRecord(evk1(k), st));
-  }
+  CKI(host_pipeline(ctx, host, 0, dims.w0, dtype, dims, bounds, nchunks, affine, am, nbins,
+                    ctx->hist.as<int64_t>(), timings));
+  if (affine) CKI(read_flags(ctx, st));
   BinResult r;
-  if (rc == ECC_OK) {
-    rc = finalize_to_host(ctx, (uint32_t)nbins, st, &r);
-  }
-  CKR(cudaStreamSynchronize(cp));
-  CKR(cudaStreamSynchronize(st));
-  if (rc == ECC_OK && timings) {
-    for (size_t k = 0; k < nchunks; ++k) {
-      float a = 0, b = 0, c = 0, d = 0;
-      CKR(cudaEventElapsedTime(&a, start, evh0(k)));
-      CKR(cudaEventElapsedTime(&b, start, evh1(k)));
-      CKR(cudaEventElapsedTime(&c, start, evk0(k)));
-      CKR(cudaEventElapsedTime(&d, start, evk1(k)));
-      ecc_chunk_timing& t = timings[k];
-      t.begin = bounds[k];
-      t.end = bounds[k + 1];
-      t.ingest_begin = t_start + a * 1e-3;
-      t.ingest_end = t_start + b * 1e-3;
-      t.index_begin = t.index_end = t.ingest_end;
-      t.kernel_begin = t_start + c * 1e-3;
-      t.kernel_end = t_start + d * 1e-3;
-      t.merge_begin = t.merge_end = t.kernel_end;
-    }
-  }
-  for (auto& e : ev) cudaEventDestroy(e);
-  if (rc != ECC_OK) return rc;
+  CKI(finalize_to_host(ctx, (uint32_t)nbins, st, &r));
   const size_t m = r.changes.size();
   *n_out = m;
   if (m > cap) return fail(ECC_EINVAL, "output capacity below the number of values");
   write_values(dtype, false, am, r, values_out);
   std::memcpy(changes_out, r.changes.data(), m * 8);
+  return ECC_OK;
+}
+
+int ecc_accumulate_host(ecc_ctx* ctx, const void* host_planes, uint64_t plane0,
+                        uint64_t nplanes, ecc_dtype dtype, ecc_dims image,
+                        const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
+                        int64_t* d_hist) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_dims(image));
+  if (!host_planes || !bounds || !d_hist) return fail(ECC_EINVAL, "null pointer");
+  if (nchunks == 0) return fail(ECC_EINVAL, "empty chunk plan");
+  for (size_t k = 0; k < nchunks; ++k)
+    if (bounds[k + 1] <= bounds[k] || bounds[k + 1] > image.w0)
+      return fail(ECC_EINVAL, "chunk bounds must increase within [0, w0]");
+  uint64_t nbins = 0;
+  bool affine = false, sorted = false;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  if (sorted) return fail(ECC_EINVAL, "the sorted bin map has no dense histogram");
+  CKI(ctx->flags.ensure(4));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, ctx->stream));
+  CKI(host_pipeline(ctx, host_planes, plane0, nplanes, dtype, image, bounds, nchunks, affine, am,
+                    nbins, d_hist, nullptr));
+  if (affine) CKI(read_flags(ctx, ctx->stream));
   return ECC_OK;
 }
 

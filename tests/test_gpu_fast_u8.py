@@ -143,3 +143,39 @@ def test_overlapped_host_input(ctx, shape):
     _check(ctx, img)
     c = ctx.curve(img)
     assert int(c.chi[-1]) == 1
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_sharded_host_streaming(ctx, world):
+    """ecc_accumulate_host (C5 on several GPUs): each "rank" streams only its
+    planes + halos from its own host buffer, chunk by chunk; the summed
+    histograms finalize to the oracle's curve (u8 and u16)."""
+    import torch
+    from paper_2203_09087_b200.shard import shard_bounds
+    rng = np.random.default_rng(40 + world)
+    for dt, hi, nb in ((np.uint8, 256, 256), (np.uint16, 65536, 65536)):
+        img = rng.integers(0, hi, (45, 40, 48), dtype=dt)
+        dims = eb.Dims.of(img.shape)
+        total = torch.zeros(2 * nb, dtype=torch.int64, device="cuda")
+        for r in range(world):
+            sh = shard_bounds(img.shape[0], world, r)
+            mine = np.ascontiguousarray(img[sh.plane0:sh.plane1])
+            n = sh.own1 - sh.own0
+            bounds = sorted({sh.own0 + n * k // 3 for k in range(4)})
+            h = torch.zeros(2 * nb, dtype=torch.int64, device="cuda")
+            ctx.accumulate_host(mine, sh.plane0, dims, bounds, h)
+            total += h
+        bins = torch.empty(nb, dtype=torch.int32, device="cuda")
+        chg = torch.empty(nb, dtype=torch.int64, device="cuda")
+        chi = torch.empty(nb, dtype=torch.int64, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+        ctx.finalize(total, nb, bins, chg, chi, cnt)
+        torch.cuda.synchronize()
+        m = int(cnt.item())
+        v, c = oracle.vcec(img)
+        assert np.array_equal(bins[:m].cpu().numpy().astype(np.int64), v.astype(np.int64))
+        assert np.array_equal(chg[:m].cpu().numpy(), c)
+    # a chunk whose halo is not in the buffer is refused
+    with pytest.raises(eb.EccError, match="host buffer holds"):
+        ctx.accumulate_host(np.zeros((5, 40, 48), np.uint8), 10, eb.Dims(45, 40, 48), [10, 15],
+                            torch.zeros(512, dtype=torch.int64, device="cuda"))
