@@ -232,6 +232,19 @@ ECC_API int ecc_batch2d(ecc_ctx* ctx, const void* data, int where, ecc_dtype dty
                 uint64_t count, uint64_t h, uint64_t w, int32_t* chi,
                 uint32_t* presence, void* stream);
 
+/* ------------------------------------------------------------ batched curve files
+ * write_curve (curve.hpp:87-121) for every image of a
+ * dense batch (ecc_batch2d's device outputs d_chi / d_presence, dtype u8 or
+ * u16 thresholds), formatted on the device: format 0 = CSV
+ * ("threshold,euler_characteristic\n" + "t,chi\n" per occurring bin),
+ * 1 = JSON ("[{"t":T,"chi":C},...]\n"), byte-identical to the reference
+ * writer.  offsets (host, count + 1) gets each image's byte range in the
+ * output and *total the size; with out == NULL the call only sizes,
+ * otherwise out (host, cap >= *total) receives the bytes. */
+ECC_API int ecc_batch_format(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t* d_presence,
+                             uint64_t count, ecc_dtype dtype, int format, char* out,
+                             uint64_t cap, uint64_t* offsets, uint64_t* total);
+
 /* ------------------------------------------------------------ synthetic inputs
  * Device fill with the reference generator (datagen.hpp:18-27): element i
  * gets counter_hash(seed, base + i) >> 56 (u8), >> 48 (u16) or

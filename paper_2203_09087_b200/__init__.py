@@ -114,6 +114,9 @@ def lib() -> C.CDLL:
             L.ecc_accumulate_host.argtypes = [_vp, _vp, _u64, _u64, C.c_int, _Dims,
                                               C.POINTER(_u64), C.c_size_t, C.POINTER(_BinMap), _vp]
             L.ecc_accumulate_host.restype = C.c_int
+            L.ecc_batch_format.argtypes = [_vp, _vp, _vp, _u64, C.c_int, C.c_int, _vp, _u64,
+                                           _vp, C.POINTER(_u64)]
+            L.ecc_batch_format.restype = C.c_int
             L.ecc_process_file.argtypes = [_vp, C.c_char_p, C.c_int, _Dims, C.c_int, C.POINTER(_u64),
                                            C.c_size_t, C.POINTER(_BinMap), C.POINTER(_Timing), _vp,
                                            _vp, _u64, C.POINTER(_u64)]
@@ -696,6 +699,22 @@ class Context:
         _check(lib().ecc_bench_run(self._p, _Dims(dims.w0, dims.w1, dims.w2), iterations, seed,
                                    sigma, width, C.byref(r)))
         return BenchReport(**{f: getattr(r, f) for f, _ in _BenchReport._fields_})
+
+    def batch_format(self, chi, presence, dtype=np.uint16, fmt: str = "csv"):
+        """write_curve bytes (curve.hpp:87-121) of every image of a device
+        batch (batch2d's chi / presence tensors), formatted on the GPU:
+        returns one bytes object per image."""
+        dt = _DT[np.dtype(dtype)]
+        count = chi.shape[0]
+        f = {"csv": 0, "json": 1}[fmt]
+        offs = np.empty(count + 1, np.uint64)
+        total = _u64()
+        _check(lib().ecc_batch_format(self._p, chi.data_ptr(), presence.data_ptr(), count, dt, f,
+                                      None, 0, offs.ctypes.data, C.byref(total)))
+        out = np.empty(max(1, total.value), np.uint8)
+        _check(lib().ecc_batch_format(self._p, chi.data_ptr(), presence.data_ptr(), count, dt, f,
+                                      out.ctypes.data, out.size, offs.ctypes.data, C.byref(total)))
+        return [out[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(count)]
 
     def fill_synthetic(self, tensor, seed: int = 1, base: int = 0, stream: int = 0):
         import torch

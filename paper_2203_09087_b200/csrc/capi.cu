@@ -1508,4 +1508,42 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
   return ECC_OK;
 }
 
+int ecc_batch_format(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t* d_presence,
+                     uint64_t count, ecc_dtype dtype, int format, char* out, uint64_t cap,
+                     uint64_t* offsets, uint64_t* total) {
+  CKI(bind(ctx));
+  if (dtype != ECC_U8 && dtype != ECC_U16)
+    return fail(ECC_EINVAL, "batched curves have u8 or u16 thresholds");
+  if (format != 0 && format != 1) return fail(ECC_EINVAL, "format must be 0 (csv) or 1 (json)");
+  if (!d_chi || !d_presence || !offsets || !total) return fail(ECC_EINVAL, "null pointer");
+  const uint32_t nbins = dtype == ECC_U8 ? 256 : 65536;
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->sums.ensure((count + 1) * 8));
+  CKI(ctx->sums2.ensure((count + 1) * 8));
+  uint64_t* sizes = ctx->sums.as<uint64_t>();
+  uint64_t* offs = ctx->sums2.as<uint64_t>();
+  CKR(cudaMemsetAsync(sizes + count, 0, 8, st));
+  CKR(launch_format_sizes(d_chi, d_presence, count, nbins, format, sizes, st));
+  size_t t = 0;
+  CKR(cub::DeviceScan::ExclusiveSum(nullptr, t, sizes, offs, (int)(count + 1), st));
+  CKI(ctx->tmp.ensure(t));
+  t = ctx->tmp.cap;
+  CKR(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, t, sizes, offs, (int)(count + 1), st));
+  CKR(cudaMemcpyAsync(offsets, offs, (count + 1) * 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  ctx->launches += 2;
+  *total = offsets[count];
+  if (!out) return ECC_OK;  // size query
+  if (cap < *total)
+    return fail(ECC_EINVAL, "output capacity " + std::to_string(cap) + " is below the " +
+                                std::to_string(*total) + " bytes");
+  CKI(ctx->keys.ensure(*total));
+  CKR(launch_format_write(d_chi, d_presence, count, nbins, format, offs, ctx->keys.as<char>(),
+                          st));
+  ctx->launches += 1;
+  CKR(cudaMemcpyAsync(out, ctx->keys.p, *total, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
 }  // extern "C"

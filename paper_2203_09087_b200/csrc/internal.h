@@ -73,6 +73,12 @@ int gaussian_max_width();
 cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint64_t w1,
                                  uint64_t w2, int axis, const double* d_weights, int width,
                                  cudaStream_t st);
+// batched curve serialisation (k_format.cu)
+cudaError_t launch_format_sizes(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                uint32_t nbins, int json, uint64_t* sizes, cudaStream_t st);
+cudaError_t launch_format_write(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                uint32_t nbins, int json, const uint64_t* offsets, char* out,
+                                cudaStream_t st);
 cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
                         uint64_t base, int sms, cudaStream_t st);
 

@@ -1,0 +1,176 @@
+// k_format.cu -- curve serialisation on the device for batched curves
+// (SURVEY.md 8(f) rank 4): write_curve's CSV and JSON layouts
+// (curve.hpp:87-121) for every image of a dense batch (ecc_batch2d output:
+// int32 chi[count][nbins] + presence bitmaps), byte-identical to the
+// reference writer.  Thresholds of u8 / u16 curves are integers, so
+// format_value (curve.hpp:56-66) is plain decimal (std::to_chars of an
+// int64); no shortest-float formatting is needed.
+//
+// Two passes, one CTA per image: k_format_sizes sums the bytes of the
+// image's occurring points (block reduction); after an exclusive scan over
+// images, k_format_write block-scans the per-thread byte counts and entry
+// counts and each thread writes its run of lines.
+#include <cub/cub.cuh>
+
+#include "internal.h"
+
+namespace eccb {
+namespace fmt {
+
+constexpr int NT = 512;
+
+__device__ __forceinline__ int ndigits_u(uint32_t v) {
+  int n = 1;
+  while (v >= 10) {
+    v /= 10;
+    ++n;
+  }
+  return n;
+}
+
+__device__ __forceinline__ int len_i(int32_t v) {
+  const uint32_t a = v < 0 ? (uint32_t)(-(int64_t)v) : (uint32_t)v;
+  return ndigits_u(a) + (v < 0);
+}
+
+__device__ __forceinline__ char* put_u(char* p, uint32_t v) {
+  const int n = ndigits_u(v);
+  for (int i = n - 1; i >= 0; --i) {
+    p[i] = (char)('0' + v % 10);
+    v /= 10;
+  }
+  return p + n;
+}
+
+__device__ __forceinline__ char* put_i(char* p, int32_t v) {
+  if (v < 0) {
+    *p++ = '-';
+    return put_u(p, (uint32_t)(-(int64_t)v));
+  }
+  return put_u(p, (uint32_t)v);
+}
+
+__device__ __forceinline__ char* put_s(char* p, const char* s) {
+  while (*s) *p++ = *s++;
+  return p;
+}
+
+// bytes of one point: CSV "t,chi\n"; JSON "{"t":T,"chi":C}" (+ "," before
+// every point but the first, counted by the writer)
+__device__ __forceinline__ int point_bytes(int json, uint32_t t, int32_t c) {
+  return json ? 5 + ndigits_u(t) + 7 + len_i(c) + 1 : ndigits_u(t) + 1 + len_i(c) + 1;
+}
+
+constexpr int CSV_HEADER = 31;  // "threshold,euler_characteristic\n"
+
+__global__ void __launch_bounds__(NT) k_format_sizes(const int32_t* __restrict__ chi,
+                                                     const uint32_t* __restrict__ pres,
+                                                     uint32_t nbins, int json,
+                                                     uint64_t* __restrict__ sizes) {
+  const int32_t* row = chi + (size_t)blockIdx.x * nbins;
+  const uint32_t* prow = pres + (size_t)blockIdx.x * (nbins / 32);
+  const uint32_t per = (nbins + NT - 1) / NT;
+  const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
+  uint64_t bytes = 0, pts = 0;
+  for (uint32_t b = b0; b < b1; ++b)
+    if ((prow[b >> 5] >> (b & 31)) & 1u) {
+      bytes += point_bytes(json, b, row[b]);
+      ++pts;
+    }
+  using Red = cub::BlockReduce<ulonglong2, NT>;
+  __shared__ typename Red::TempStorage tmp;
+  struct Add {
+    __device__ ulonglong2 operator()(const ulonglong2& a, const ulonglong2& b) const {
+      return make_ulonglong2(a.x + b.x, a.y + b.y);
+    }
+  };
+  const ulonglong2 tot = Red(tmp).Reduce(make_ulonglong2(bytes, pts), Add());
+  if (threadIdx.x == 0) {
+    uint64_t total = tot.x;
+    if (json)
+      total += 1 + (tot.y > 1 ? tot.y - 1 : 0) + 2;  // '[' , commas , "]\n"
+    else
+      total += CSV_HEADER;
+    sizes[blockIdx.x] = total;
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_format_write(const int32_t* __restrict__ chi,
+                                                     const uint32_t* __restrict__ pres,
+                                                     uint32_t nbins, int json,
+                                                     const uint64_t* __restrict__ offsets,
+                                                     char* __restrict__ out) {
+  const int32_t* row = chi + (size_t)blockIdx.x * nbins;
+  const uint32_t* prow = pres + (size_t)blockIdx.x * (nbins / 32);
+  const uint32_t per = (nbins + NT - 1) / NT;
+  const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
+  uint64_t bytes = 0, pts = 0;
+  for (uint32_t b = b0; b < b1; ++b)
+    if ((prow[b >> 5] >> (b & 31)) & 1u) {
+      bytes += point_bytes(json, b, row[b]);
+      ++pts;
+    }
+  using Scan = cub::BlockScan<ulonglong2, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  struct Add {
+    __device__ ulonglong2 operator()(const ulonglong2& a, const ulonglong2& b) const {
+      return make_ulonglong2(a.x + b.x, a.y + b.y);
+    }
+  };
+  ulonglong2 ex;
+  Scan(tmp).ExclusiveScan(make_ulonglong2(bytes, pts), ex, make_ulonglong2(0, 0), Add());
+  char* base = out + offsets[blockIdx.x];
+  const uint64_t head = json ? 1 : CSV_HEADER;
+  if (threadIdx.x == 0) {
+    if (json)
+      base[0] = '[';
+    else
+      put_s(base, "threshold,euler_characteristic\n");
+  }
+  // every point but the image's first is preceded by a comma in JSON: the
+  // ex.y - 1 commas before this thread's first point lie ahead of it (that
+  // point's own comma is written below)
+  char* p = base + head + ex.x + ((json && ex.y > 0) ? ex.y - 1 : 0);
+  uint64_t idx = ex.y;
+  for (uint32_t b = b0; b < b1; ++b)
+    if ((prow[b >> 5] >> (b & 31)) & 1u) {
+      if (json) {
+        if (idx > 0) *p++ = ',';
+        p = put_s(p, "{\"t\":");
+        p = put_u(p, b);
+        p = put_s(p, ",\"chi\":");
+        p = put_i(p, row[b]);
+        *p++ = '}';
+      } else {
+        p = put_u(p, b);
+        *p++ = ',';
+        p = put_i(p, row[b]);
+        *p++ = '\n';
+      }
+      ++idx;
+    }
+  if (json && threadIdx.x == NT - 1) {
+    char* end = out + offsets[blockIdx.x + 1];
+    end[-2] = ']';
+    end[-1] = '\n';
+  }
+}
+
+}  // namespace fmt
+
+cudaError_t launch_format_sizes(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                uint32_t nbins, int json, uint64_t* sizes, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  fmt::k_format_sizes<<<(unsigned)count, fmt::NT, 0, st>>>(chi, pres, nbins, json, sizes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_format_write(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                uint32_t nbins, int json, const uint64_t* offsets, char* out,
+                                cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  fmt::k_format_write<<<(unsigned)count, fmt::NT, 0, st>>>(chi, pres, nbins, json, offsets, out);
+  return cudaGetLastError();
+}
+
+}  // namespace eccb
