@@ -245,6 +245,14 @@ ECC_API int ecc_batch_format(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t*
                              uint64_t count, ecc_dtype dtype, int format, char* out,
                              uint64_t cap, uint64_t* offsets, uint64_t* total);
 
+/* zero_crossings (curve.hpp:36-50) of every image of a dense batch, on the
+ * device: bit t of d_out[b] (uint32[count][nbins/32]) is set iff occurring
+ * bin t of image b has chi == 0 or a strict sign change from the image's
+ * previous occurring point. */
+ECC_API int ecc_batch_zero_crossings(ecc_ctx* ctx, const int32_t* d_chi,
+                                     const uint32_t* d_presence, uint64_t count, ecc_dtype dtype,
+                                     uint32_t* d_out, void* stream);
+
 /* ------------------------------------------------------------ synthetic inputs
  * Device fill with the reference generator (datagen.hpp:18-27): element i
  * gets counter_hash(seed, base + i) >> 56 (u8), >> 48 (u16) or

@@ -117,6 +117,8 @@ def lib() -> C.CDLL:
             L.ecc_batch_format.argtypes = [_vp, _vp, _vp, _u64, C.c_int, C.c_int, _vp, _u64,
                                            _vp, C.POINTER(_u64)]
             L.ecc_batch_format.restype = C.c_int
+            L.ecc_batch_zero_crossings.argtypes = [_vp, _vp, _vp, _u64, C.c_int, _vp, _vp]
+            L.ecc_batch_zero_crossings.restype = C.c_int
             L.ecc_process_file.argtypes = [_vp, C.c_char_p, C.c_int, _Dims, C.c_int, C.POINTER(_u64),
                                            C.c_size_t, C.POINTER(_BinMap), C.POINTER(_Timing), _vp,
                                            _vp, _u64, C.POINTER(_u64)]
@@ -715,6 +717,18 @@ class Context:
         _check(lib().ecc_batch_format(self._p, chi.data_ptr(), presence.data_ptr(), count, dt, f,
                                       out.ctypes.data, out.size, offs.ctypes.data, C.byref(total)))
         return [out[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(count)]
+
+    def batch_zero_crossings(self, chi, presence, dtype=np.uint16, out=None, stream: int = 0):
+        """zero_crossings (curve.hpp:36-50) of every image of a device batch:
+        a (count, nbins/32) int32 bitmap tensor (bit t = occurring bin t is
+        a zero crossing)."""
+        import torch
+        dt = _DT[np.dtype(dtype)]
+        if out is None:
+            out = torch.empty_like(presence)
+        _check(lib().ecc_batch_zero_crossings(self._p, chi.data_ptr(), presence.data_ptr(),
+                                              chi.shape[0], dt, out.data_ptr(), stream or None))
+        return out
 
     def fill_synthetic(self, tensor, seed: int = 1, base: int = 0, stream: int = 0):
         import torch

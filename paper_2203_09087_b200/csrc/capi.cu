@@ -1546,4 +1546,16 @@ int ecc_batch_format(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t* d_prese
   return ECC_OK;
 }
 
+int ecc_batch_zero_crossings(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t* d_presence,
+                             uint64_t count, ecc_dtype dtype, uint32_t* d_out, void* stream) {
+  CKI(bind(ctx));
+  if (dtype != ECC_U8 && dtype != ECC_U16)
+    return fail(ECC_EINVAL, "batched curves have u8 or u16 thresholds");
+  if (!d_chi || !d_presence || !d_out) return fail(ECC_EINVAL, "null device pointer");
+  CKR(launch_zero_crossings(d_chi, d_presence, count, dtype == ECC_U8 ? 256 : 65536, d_out,
+                            pick(ctx, stream)));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
 }  // extern "C"

@@ -79,6 +79,8 @@ cudaError_t launch_format_sizes(const int32_t* chi, const uint32_t* pres, uint64
 cudaError_t launch_format_write(const int32_t* chi, const uint32_t* pres, uint64_t count,
                                 uint32_t nbins, int json, const uint64_t* offsets, char* out,
                                 cudaStream_t st);
+cudaError_t launch_zero_crossings(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                  uint32_t nbins, uint32_t* zc, cudaStream_t st);
 cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
                         uint64_t base, int sms, cudaStream_t st);
 

@@ -156,7 +156,52 @@ __global__ void __launch_bounds__(NT) k_format_write(const int32_t* __restrict__
   }
 }
 
+// zero_crossings (curve.hpp:36-50) of every image: bit t of the output row is
+// set iff occurring bin t is a zero crossing -- chi == 0, or a strict sign
+// change from the previous occurring point (which may lie in another
+// thread's range: a block scan carries the last occurring chi forward).
+// Thread ranges are whole bitmap words (>= 32 bins).
+__global__ void __launch_bounds__(NT) k_zero_crossings(const int32_t* __restrict__ chi,
+                                                       const uint32_t* __restrict__ pres,
+                                                       uint32_t nbins, uint32_t* __restrict__ zc) {
+  const int32_t* row = chi + (size_t)blockIdx.x * nbins;
+  const uint32_t* prow = pres + (size_t)blockIdx.x * (nbins / 32);
+  uint32_t* zrow = zc + (size_t)blockIdx.x * (nbins / 32);
+  const uint32_t per = max(32u, (nbins + NT - 1) / NT / 32 * 32);
+  const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
+  // (has a point, chi of the last point) of this thread's range
+  int2 last = make_int2(0, 0);
+  for (uint32_t b = b0; b < b1; ++b)
+    if ((prow[b >> 5] >> (b & 31)) & 1u) last = make_int2(1, row[b]);
+  struct Last {
+    __device__ int2 operator()(const int2& a, const int2& b) const { return b.x ? b : a; }
+  };
+  using Scan = cub::BlockScan<int2, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  int2 prev;
+  Scan(tmp).ExclusiveScan(last, prev, make_int2(0, 0), Last());
+  for (uint32_t w = b0; w < b1; w += 32) {
+    uint32_t bits = 0;
+    const uint32_t pw = prow[w >> 5];
+    for (uint32_t j = 0; j < 32 && w + j < b1; ++j)
+      if ((pw >> j) & 1u) {
+        const int32_t c = row[w + j];
+        const bool z = c == 0 || (prev.x && prev.y != 0 && ((c > 0) != (prev.y > 0)));
+        bits |= (uint32_t)z << j;
+        prev = make_int2(1, c);
+      }
+    zrow[w >> 5] = bits;
+  }
+}
+
 }  // namespace fmt
+
+cudaError_t launch_zero_crossings(const int32_t* chi, const uint32_t* pres, uint64_t count,
+                                  uint32_t nbins, uint32_t* zc, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  fmt::k_zero_crossings<<<(unsigned)count, fmt::NT, 0, st>>>(chi, pres, nbins, zc);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_format_sizes(const int32_t* chi, const uint32_t* pres, uint64_t count,
                                 uint32_t nbins, int json, uint64_t* sizes, cudaStream_t st) {

@@ -60,3 +60,30 @@ def test_batch_format_c3_scale(ctx):
         t, c = eb.curve_batch_to_points(chi[b].cpu().numpy(), pres[b].cpu().numpy().view(np.uint32))
         assert files[b] == _csv(t, c)
         assert oracle.curve_digest(t, c) == gold[f"C3_{b}"]["digest"]
+
+
+def _zero_crossings(t, chi):
+    out = []
+    for i in range(len(t)):
+        if chi[i] == 0:
+            out.append(int(t[i]))
+        elif i > 0 and chi[i - 1] != 0 and (chi[i] > 0) != (chi[i - 1] > 0):
+            out.append(int(t[i]))
+    return out
+
+
+@pytest.mark.parametrize("dt,hi,shape", [(np.uint8, 256, (9, 40, 40)), (np.uint16, 65536, (4, 96, 96)),
+                                          (np.uint16, 300, (6, 50, 70)), (np.uint8, 6, (5, 12, 12))])
+def test_batch_zero_crossings(ctx, dt, hi, shape):
+    """zero_crossings (curve.hpp:36-50) on the device == its restatement."""
+    import torch
+    rng = np.random.default_rng(hi + 1)
+    imgs = rng.integers(0, hi, shape).astype(dt)
+    chi, pres = ctx.batch2d(torch.from_numpy(imgs).cuda())
+    zc = ctx.batch_zero_crossings(chi, pres, dt)
+    torch.cuda.synchronize()
+    chi_h, pres_h, zc_h = chi.cpu().numpy(), pres.cpu().numpy().view(np.uint32), zc.cpu().numpy().view(np.uint32)
+    for b in range(shape[0]):
+        t, c = eb.curve_batch_to_points(chi_h[b], pres_h[b])
+        bits = np.unpackbits(zc_h[b].view(np.uint8), bitorder="little").astype(bool)
+        assert list(np.nonzero(bits)[0]) == _zero_crossings(t, c), b
