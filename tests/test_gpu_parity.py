@@ -414,3 +414,16 @@ def test_u16_spill_path_isolated_minima(ctx):
     assert np.array_equal(got.values.astype(np.int64), v.astype(np.int64))
     assert np.array_equal(got.changes, c)
     assert got.changes[0] == 256 ** 3
+
+
+def test_f32_sorted_2d_infinities_and_signed_zeros(ctx):
+    """The reference's quirks on the sorted f32 path in 2D:
+    +inf pixels tie with the +inf collar sentinel, -0 merges into +0."""
+    rng = np.random.default_rng(77)
+    for shape in [(30, 41), (1, 50), (64, 1)]:
+        img = rng.choice(np.array([-np.inf, -1.5, -0.0, 0.0, 2.0, np.inf], np.float32),
+                         size=shape)
+        a = ctx.vcec(img)
+        assert _same(a.values, a.changes, *oracle.vcec(img)), shape
+        if oracle.ref_available():
+            assert _same(a.values, a.changes, *oracle.ref_vcec(img)), shape
