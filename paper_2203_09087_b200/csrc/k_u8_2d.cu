@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
 bool u8_2d_supported(const Slab& s) {
   return s.w2 == 1 && s.w1 >= 1 && s.plane_pitch() % 16 == 0 &&
          (reinterpret_cast<uintptr_t>(s.base) % 16) == 0 && s.w0 < (1ll << 31) &&
-         s.w1 < (1ll << 31) - 64 && (s.own1 - s.own0) * s.w1 < (1ll << 40);
+         s.w1 < (1ll << 31) - 64 && (s.own1 - s.own0) * s.w1 < (1ll << 38);  // u32 per-CTA counts
 }
 
 cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st,
