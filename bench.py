@@ -5,8 +5,12 @@ rank owns a 512^3 u8 z-slab (axis-0 planes [512 r, 512 r + 512)) of a
 (512 N) x 512 x 512 synthetic volume (v = counter_hash(1,
 i) >> 56), plus one halo plane from each neighbouring slab.  One step at
 N = 1 is ONE fused launch (ecc_curve_device: stencil + histogram + the last
-CTA's compaction + prefix sum); at N > 1 it is K1+K2 over the slab, one NCCL
-all-reduce of the 2 x 256 int64 histogram, and K3.  Per-GPU work is fixed as
+CTA's compaction + prefix sum); at N > 1 it is also ONE launch per rank
+(ecc_curve_sharded): K1+K2 over the slab, then the last CTA stores the rank's
+2 x 256 int64 histogram into every peer's exchange buffer over NVLink (CUDA
+IPC), waits for all ranks and runs K3 on the sum -- the all-reduce fused into
+the kernel; NCCL all-reduce + K3 is the fallback (--no-p2p, or when the peer
+mappings cannot be opened).  Per-GPU work is fixed as
 N grows ("scaling": "weak").
 
 * value     -- device-resident voxels/s (inputs already in HBM), CUDA events
@@ -142,6 +146,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-p2p", action="store_true",
+                    help="N > 1: NCCL all-reduce instead of the exchange fused into the launch")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N > 1 path on a box with fewer GPUs "
@@ -204,8 +210,59 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
+    # N > 1: the histogram exchange fused into the stencil launch over peer
+    # memory (ecc_curve_sharded, CUDA IPC + NVLink stores); NCCL all-reduce
+    # if the peer mappings cannot be set up or disagree with it
+    xchg = None
+    exchange = "none" if dist is None else "nccl_allreduce"
+    if dist is not None and not args.no_p2p:
+        try:
+            x = eb.Exchange(ctx, rank, world)
+            handles = [None] * world
+            dist.all_gather_object(handles, x.handle)
+            x.open(handles)
+            ref = []
+            for use in (None, x):  # one NCCL step, one fused step: same curve?
+                with torch.cuda.stream(stream):
+                    if use is None:
+                        hist.zero_()
+                        sharded_histogram(sh, lambda shd, h: ctx.accumulate_slab(
+                            slab, dims, shd.plane0, shd.own0, shd.own1, h, stream=ctx.stream),
+                            hist, dist.all_reduce)
+                        ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
+                    else:
+                        ctx.curve_sharded(x, slab, dims, p0, own0, own1, bins, chg, chi, cnt,
+                                          stream=ctx.stream)
+                torch.cuda.synchronize()
+                if use is not None:
+                    x.status()
+                ref.append((cnt.clone(), chi.clone(), bins.clone()))
+            same = all(torch.equal(a, b) for a, b in zip(ref[0], ref[1]))
+            agree = torch.tensor([1 if same else 0], device=dev)
+            dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+            if int(agree.item()) == 1:
+                xchg, exchange = x, "p2p_fused_exchange"
+            else:
+                x.close()
+        except Exception as e:  # fall back to NCCL, reported in the JSON
+            exchange = f"nccl_allreduce (p2p setup failed: {str(e)[:80]})"
+        flag = torch.tensor([1 if xchg is not None else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and xchg is not None:  # every rank must agree
+            xchg.close()
+            xchg, exchange = None, "nccl_allreduce"
+
     def step(ev_k0=None, ev_k1=None):
         with torch.cuda.stream(stream):
+            if xchg is not None:
+                # K1+K2 + exchange over peer memory + K3: ONE launch
+                if ev_k0 is not None:
+                    ev_k0.record(stream)
+                ctx.curve_sharded(xchg, slab, dims, p0, own0, own1, bins, chg, chi, cnt,
+                                  stream=ctx.stream)
+                if ev_k1 is not None:
+                    ev_k1.record(stream)
+                return
             if dist is None:
                 # whole volume on one GPU: ONE fused launch (K1+K2+K3)
                 if ev_k0 is not None:
@@ -293,10 +350,14 @@ def main():
             t0 = time.perf_counter()
             with torch.cuda.stream(stream):
                 buf.copy_(host, non_blocking=True)
-                hist.zero_()
-                ctx.accumulate_slab(buf, dims, p0, own0, own1, hist, stream=ctx.stream)
-                dist.all_reduce(hist)
-                ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
+                if xchg is not None:
+                    ctx.curve_sharded(xchg, buf, dims, p0, own0, own1, bins, chg, chi, cnt,
+                                      stream=ctx.stream)
+                else:
+                    hist.zero_()
+                    ctx.accumulate_slab(buf, dims, p0, own0, own1, hist, stream=ctx.stream)
+                    dist.all_reduce(hist)
+                    ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
                 hcur[0].copy_(bins.to(torch.int64), non_blocking=True)
                 hcur[1].copy_(chi, non_blocking=True)
             stream.synchronize()
@@ -328,7 +389,7 @@ def main():
            "data": "synthetic (counter_hash seed 1, SURVEY.md 8(d)); device-generated",
            "config": {"workload": "C2: 512^3 u8 3D ECC per GPU (z-slab of a (512N)x512x512 volume)",
                       "voxels_per_gpu": SIDE ** 3, "bins": 256,
-                      "parallelism": f"zslab{n}" + (f"+{args.dist_backend}_allreduce" if n > 1 else ""),
+                      "parallelism": f"zslab{n}" + (f"+{exchange}" if n > 1 else ""),
                       "l2": "flushed between timed steps (256 MiB write)"},
            "kernel_ms": t_kern,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -345,6 +406,8 @@ def main():
             out["cpu_baseline"] = {"value": None, "error": str(e)[:200]}
     if rank == 0:
         print(json.dumps(out), flush=True)
+    if xchg is not None:
+        xchg.close()
     if dist is not None:
         dist.destroy_process_group()
 

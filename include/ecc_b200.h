@@ -221,6 +221,30 @@ ECC_API int ecc_accumulate_host(ecc_ctx* ctx, const void* host_planes, uint64_t 
                                 const uint64_t* bounds, size_t nchunks, const ecc_binmap* bm,
                                 int64_t* d_hist);
 
+/* ------------------------------------------------------------ fused multi-GPU exchange
+ * z-slab sharding with the all-reduce fused into the stencil
+ * launch.  Each rank creates an exchange buffer (ecc_xchg_create; the 64-byte
+ * CUDA-IPC handle it returns is all-gathered by the caller, e.g. through
+ * torch.distributed), opens its peers' buffers (ecc_xchg_open), then
+ * ecc_curve_sharded runs K1+K2 over its slab and, in the same launch, the
+ * last CTA stores the rank's histogram into every peer's buffer over NVLink,
+ * waits for all ranks and runs K3 on the sum: every rank ends with the
+ * global curve in d_bins / d_changes / d_chi / d_count (as ecc_curve_device).
+ * 3D u8 slabs (the C2 path).  All ranks must call ecc_curve_sharded the same
+ * number of times; ecc_xchg_status reports a peer that never arrived (10 s
+ * guard inside the kernel instead of a hang).  Replaces the reference's
+ * per-chunk merge_local (vcec.hpp:35-66) across devices. */
+typedef struct ecc_xchg ecc_xchg;
+ECC_API int ecc_xchg_create(ecc_ctx* ctx, int rank, int world, ecc_xchg** out,
+                            void* handle_out /* 64 bytes */);
+ECC_API int ecc_xchg_open(ecc_xchg* x, const void* handles /* world x 64 bytes */);
+ECC_API void ecc_xchg_destroy(ecc_xchg* x);
+ECC_API int ecc_xchg_status(ecc_xchg* x);
+ECC_API int ecc_curve_sharded(ecc_ctx* ctx, ecc_xchg* x, const void* d_planes, ecc_dims image,
+                              uint64_t plane0, uint64_t nplanes, uint64_t own0, uint64_t own1,
+                              uint32_t* d_bins, int64_t* d_changes, int64_t* d_chi,
+                              uint64_t* d_count, void* stream);
+
 /* ------------------------------------------------------------ batched 2D
  * New entry point (the reference has none): `count` images of
  * h x w (axis 0 = h), stored back to back.  For each image b, writes the

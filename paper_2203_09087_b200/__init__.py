@@ -119,6 +119,17 @@ def lib() -> C.CDLL:
             L.ecc_batch_format.restype = C.c_int
             L.ecc_batch_zero_crossings.argtypes = [_vp, _vp, _vp, _u64, C.c_int, _vp, _vp]
             L.ecc_batch_zero_crossings.restype = C.c_int
+            L.ecc_xchg_create.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_vp), _vp]
+            L.ecc_xchg_create.restype = C.c_int
+            L.ecc_xchg_open.argtypes = [_vp, _vp]
+            L.ecc_xchg_open.restype = C.c_int
+            L.ecc_xchg_destroy.argtypes = [_vp]
+            L.ecc_xchg_destroy.restype = None
+            L.ecc_xchg_status.argtypes = [_vp]
+            L.ecc_xchg_status.restype = C.c_int
+            L.ecc_curve_sharded.argtypes = [_vp, _vp, _vp, _Dims, _u64, _u64, _u64, _u64,
+                                            _vp, _vp, _vp, _vp, _vp]
+            L.ecc_curve_sharded.restype = C.c_int
             L.ecc_process_file.argtypes = [_vp, C.c_char_p, C.c_int, _Dims, C.c_int, C.POINTER(_u64),
                                            C.c_size_t, C.POINTER(_BinMap), C.POINTER(_Timing), _vp,
                                            _vp, _u64, C.POINTER(_u64)]
@@ -645,6 +656,16 @@ class Context:
                                       C.byref(bm), bins.data_ptr(), changes.data_ptr(),
                                       chi.data_ptr(), count.data_ptr(), stream or None))
 
+    def curve_sharded(self, xchg: "Exchange", planes, dims: Dims, plane0: int, own0: int,
+                      own1: int, bins, changes, chi, count, stream: int = 0):
+        """ecc_curve_sharded: this rank's slab -> the GLOBAL curve on every
+        rank, the histogram exchange fused into the launch (see Exchange)."""
+        nplanes = planes.numel() // (dims.w1 * dims.w2)
+        _check(lib().ecc_curve_sharded(self._p, xchg._p, planes.data_ptr(),
+                                       _Dims(dims.w0, dims.w1, dims.w2), plane0, nplanes, own0,
+                                       own1, bins.data_ptr(), changes.data_ptr(), chi.data_ptr(),
+                                       count.data_ptr(), stream or None))
+
     def finalize(self, hist, nbins: int, bins, changes, chi, count, stream: int = 0):
         _check(lib().ecc_finalize(self._p, hist.data_ptr(), nbins, bins.data_ptr(),
                                   changes.data_ptr(), chi.data_ptr(), count.data_ptr(),
@@ -778,6 +799,34 @@ def process_image(image, plan: ChunkPlan = None, options: EngineOptions = None,
             return ctx.process_host(arr, plan, report, binmap)
         return ctx.process_source(MemorySource(image), plan, options, report, binmap)
     return ctx.vcec(image, binmap)
+
+
+class Exchange:
+    """Fused multi-GPU rank exchange (ecc_xchg_*): create on every rank,
+    all-gather `handle` (64 bytes), `open(handles)`, then
+    Context.curve_sharded(...) runs K1+K2 over the rank's slab and the
+    histogram exchange over peer memory + K3 in ONE launch."""
+
+    def __init__(self, ctx: "Context", rank: int, world: int):
+        self.ctx = ctx
+        self._p = C.c_void_p()
+        h = C.create_string_buffer(64)
+        _check(lib().ecc_xchg_create(ctx._p, rank, world, C.byref(self._p), h))
+        self.handle = h.raw
+        self.world = world
+
+    def open(self, handles):
+        buf = b"".join(handles)
+        assert len(buf) == 64 * self.world
+        _check(lib().ecc_xchg_open(self._p, buf))
+
+    def status(self):
+        _check(lib().ecc_xchg_status(self._p))
+
+    def close(self):
+        if self._p:
+            lib().ecc_xchg_destroy(self._p)
+            self._p = C.c_void_p()
 
 
 def _dims_of(shape) -> _Dims:

@@ -148,6 +148,20 @@ struct ecc_ctx {
   cudaEvent_t ov_ev[17] = {};  // overlapped host-input path: start + one per chunk copy
 };
 
+// Multi-GPU rank exchange over peer memory (fin_u8.cuh, Xchg): this rank's
+// buffer -- int64 slots[2][world][512] | uint32 flags[2][world] | uint32 err
+// -- exported by CUDA IPC, the peers' buffers opened, and device arrays of
+// the peers' slot / flag pointers for the kernel.
+struct ecc_xchg {
+  ecc_ctx* ctx = nullptr;
+  int rank = 0, world = 1;
+  uint32_t epoch = 0;
+  void* buf = nullptr;
+  size_t flags_off = 0, err_off = 0, bytes = 0;
+  std::vector<void*> base;  // [world] opened peer buffers (own: buf)
+  void* ptrs = nullptr;     // device: int64_t* slots[world] | uint32_t* flags[world]
+};
+
 namespace {
 
 int bind(ecc_ctx* ctx) {
@@ -1554,6 +1568,112 @@ int ecc_batch_zero_crossings(ecc_ctx* ctx, const int32_t* d_chi, const uint32_t*
   if (!d_chi || !d_presence || !d_out) return fail(ECC_EINVAL, "null device pointer");
   CKR(launch_zero_crossings(d_chi, d_presence, count, dtype == ECC_U8 ? 256 : 65536, d_out,
                             pick(ctx, stream)));
+  ctx->launches += 1;
+  return ECC_OK;
+}
+
+int ecc_xchg_create(ecc_ctx* ctx, int rank, int world, ecc_xchg** out, void* handle_out) {
+  CKI(bind(ctx));
+  if (!out || !handle_out) return fail(ECC_EINVAL, "null pointer");
+  if (world < 1 || rank < 0 || rank >= world) return fail(ECC_EINVAL, "bad rank / world");
+  auto* x = new ecc_xchg();
+  x->ctx = ctx;
+  x->rank = rank;
+  x->world = world;
+  x->flags_off = (size_t)2 * world * 512 * 8;
+  x->err_off = x->flags_off + (size_t)2 * world * 4;
+  x->bytes = x->err_off + 256;
+  cudaError_t e = cudaMalloc(&x->buf, x->bytes);
+  if (e == cudaSuccess) e = cudaMemset(x->buf, 0, x->bytes);
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, x->buf);
+  if (e != cudaSuccess) {
+    if (x->buf) cudaFree(x->buf);
+    delete x;
+    return fail(ECC_ECUDA, std::string("exchange buffer: ") + cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle_out, &h, 64);
+  *out = x;
+  return ECC_OK;
+}
+
+int ecc_xchg_open(ecc_xchg* x, const void* handles) {
+  if (!x || !handles) return fail(ECC_EINVAL, "null pointer");
+  CKI(bind(x->ctx));
+  x->base.assign(x->world, nullptr);
+  for (int r = 0; r < x->world; ++r) {
+    if (r == x->rank) {
+      x->base[r] = x->buf;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const uint8_t*>(handles) + 64 * r, 64);
+    const cudaError_t e = cudaIpcOpenMemHandle(&x->base[r], h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ECC_ECUDA, "opening rank " + std::to_string(r) + "'s exchange buffer: " +
+                                 cudaGetErrorString(e));
+  }
+  std::vector<void*> p(2 * x->world);
+  for (int r = 0; r < x->world; ++r) {
+    p[r] = x->base[r];
+    p[x->world + r] = static_cast<uint8_t*>(x->base[r]) + x->flags_off;
+  }
+  if (!x->ptrs) CKR(cudaMalloc(&x->ptrs, p.size() * sizeof(void*)));
+  CKR(cudaMemcpy(x->ptrs, p.data(), p.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  return ECC_OK;
+}
+
+void ecc_xchg_destroy(ecc_xchg* x) {
+  if (!x) return;
+  cudaSetDevice(x->ctx->device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < (int)x->base.size(); ++r)
+    if (r != x->rank && x->base[r]) cudaIpcCloseMemHandle(x->base[r]);
+  if (x->ptrs) cudaFree(x->ptrs);
+  if (x->buf) cudaFree(x->buf);
+  delete x;
+}
+
+int ecc_xchg_status(ecc_xchg* x) {
+  if (!x) return fail(ECC_EINVAL, "null exchange");
+  CKI(bind(x->ctx));
+  uint32_t err = 0;
+  CKR(cudaStreamSynchronize(x->ctx->stream));
+  CKR(cudaMemcpy(&err, static_cast<uint8_t*>(x->buf) + x->err_off, 4, cudaMemcpyDeviceToHost));
+  if (err) return fail(ECC_ECUDA, "rank exchange timed out: a peer never published its histogram");
+  return ECC_OK;
+}
+
+int ecc_curve_sharded(ecc_ctx* ctx, ecc_xchg* x, const void* d_planes, ecc_dims image,
+                      uint64_t plane0, uint64_t nplanes, uint64_t own0, uint64_t own1,
+                      uint32_t* d_bins, int64_t* d_changes, int64_t* d_chi, uint64_t* d_count,
+                      void* stream) {
+  CKI(bind(ctx));
+  CKI(check_dims(image));
+  CKI(check_slab(image, plane0, nplanes, own0, own1));
+  if (!x || !x->ptrs) return fail(ECC_EINVAL, "exchange not opened");
+  if (!d_planes || !d_bins || !d_changes || !d_chi || !d_count)
+    return fail(ECC_EINVAL, "null device pointer");
+  const Slab s = make_slab(d_planes, image, plane0, nplanes, own0, own1);
+  if (!u8_3d_supported(s) || own1 <= own0)
+    return fail(ECC_EINVAL, "the fused sharded curve takes 3D u8 slabs with 16-byte rows");
+  cudaStream_t st = pick(ctx, stream);
+  if (!ctx->fused.p) {
+    CKI(ctx->fused.ensure(256 + 512 * 8));
+    CKR(cudaMemsetAsync(ctx->fused.p, 0, 256 + 512 * 8, st));
+  }
+  U83dFinalize fz{ctx->fused.as<uint32_t>(), d_bins, d_changes, d_chi, d_count};
+  fz.world = x->world;
+  fz.rank = x->rank;
+  fz.epoch = ++x->epoch;
+  fz.slots = static_cast<int64_t* const*>(x->ptrs);
+  fz.flags = reinterpret_cast<uint32_t* const*>(static_cast<void**>(x->ptrs) + x->world);
+  fz.my_slots = static_cast<const int64_t*>(x->buf);
+  fz.my_flags = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(x->buf) + x->flags_off);
+  fz.err = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(x->buf) + x->err_off);
+  CKR(launch_u8_3d(s, reinterpret_cast<int64_t*>(ctx->fused.as<uint8_t>() + 256), nullptr,
+                   ctx->sms, st, &fz));
   ctx->launches += 1;
   return ECC_OK;
 }

@@ -13,13 +13,46 @@
 namespace eccb {
 namespace u8fin {
 
+// Rank exchange over peer memory (multi-GPU z-slab sharding, SURVEY.md
+// 8(e)): the last CTA of every rank stores its rank's 512-entry histogram
+// into slot [parity][rank] of EVERY rank's exchange buffer (NVLink P2P
+// stores through CUDA-IPC mappings), releases a per-(parity, rank) flag
+// there, waits for all ranks' flags in its own buffer, and runs K3 on the
+// sum -- the all-reduce fused into the stencil launch.  The parity double
+// buffer keeps a rank that is one step ahead from overwriting slots a
+// slower rank is still reading.
+struct Xchg {
+  int world = 1, rank = 0;
+  uint32_t epoch = 0;           // this launch's step number (flags hold it)
+  int64_t* const* slots = nullptr;   // [world] -> peer's int64[2][world][512]
+  uint32_t* const* flags = nullptr;  // [world] -> peer's uint32[2][world]
+  const int64_t* my_slots = nullptr;
+  const uint32_t* my_flags = nullptr;
+  uint32_t* err = nullptr;      // set when a peer never arrives (timeout)
+};
+
 struct Fin {
   uint32_t* ticket;    // zero before the launch, zero again after it
   uint32_t* bins;      // [256] occurring values, ascending
   int64_t* changes;    // [256] their VCEC entries
   int64_t* chi;        // [256] the curve
   uint64_t* count;     // number of occurring values
+  Xchg x;              // world > 1: fused rank exchange
 };
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Code: static constexpr int n (codes per value in the table);
 //       static __device__ bool live(int c) (a real change, not "not emitted");
@@ -55,6 +88,38 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
   __syncthreads();
   if (!last) return;
   __threadfence();
+  const Xchg& x = fin.x;
+  const int par = (int)(x.epoch & 1u);
+  if (x.world > 1) {
+    // publish this rank's histogram into every rank's slot [par][rank]
+    for (int r = 0; r < x.world; ++r) {
+      int64_t* dst = x.slots[r] + ((size_t)par * x.world + x.rank) * 512;
+      for (int v = threadIdx.x; v < 512; v += NT) dst[v] = __ldcg(&ghist[v]);
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < x.world; ++r) st_release_sys(x.flags[r] + par * x.world + x.rank, x.epoch);
+      // wait for every rank's data in our own buffer (10 s guard: never hang)
+      const uint64_t t0 = globaltimer();
+      for (int r = 0; r < x.world; ++r)
+        while (ld_acquire_sys(x.my_flags + par * x.world + r) != x.epoch) {
+          if (globaltimer() - t0 > 10000000000ull) {
+            atomicExch(x.err, 1u);
+            break;
+          }
+        }
+    }
+    __syncthreads();
+  }
+  // the global histogram: this launch's (one rank) or the sum of all ranks'
+  auto gsum = [&](int v) -> long long {
+    if (x.world <= 1) return __ldcg(&ghist[v]);
+    long long t = 0;
+    for (int r = 0; r < x.world; ++r)
+      t += __ldcg(&x.my_slots[((size_t)par * x.world + r) * 512 + v]);
+    return t;
+  };
   // thread t owns values [VPT t, VPT (t + 1)) (VPT = 0 for threads past 256)
   constexpr int VPT = NT >= 256 ? 1 : 256 / NT;
   struct Add {
@@ -70,8 +135,8 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
   longlong2 in = make_longlong2(0, 0);
 #pragma unroll
   for (int j = 0; j < VPT; ++j) {
-    s[j] = mine ? __ldcg(&ghist[v0 + j]) : 0;
-    n[j] = mine ? __ldcg(&ghist[256 + v0 + j]) : 0;
+    s[j] = mine ? gsum(v0 + j) : 0;
+    n[j] = mine ? gsum(256 + v0 + j) : 0;
     in.x += (n[j] != 0);
     in.y += s[j];
   }

@@ -34,6 +34,14 @@ struct U83dFinalize {
   int64_t* changes;
   int64_t* chi;
   uint64_t* count;
+  // multi-GPU: fused rank exchange over peer memory (fin_u8.cuh, Xchg)
+  int world = 1, rank = 0;
+  uint32_t epoch = 0;
+  int64_t* const* slots = nullptr;   // device array [world] of peers' slot buffers
+  uint32_t* const* flags = nullptr;  // device array [world] of peers' flag arrays
+  const int64_t* my_slots = nullptr;
+  const uint32_t* my_flags = nullptr;
+  uint32_t* err = nullptr;
 };
 bool u8_3d_supported(const Slab& s);
 bool u16_3d_supported(const Slab& s);

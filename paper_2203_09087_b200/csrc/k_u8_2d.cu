@@ -246,7 +246,11 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   g.nunits = (int)units;
   const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
   u8fin::Fin fin{};
-  if (fz) fin = u8fin::Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+  if (fz) {
+    fin = u8fin::Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+    fin.x = u8fin::Xchg{fz->world, fz->rank, fz->epoch, fz->slots, fz->flags, fz->my_slots,
+                        fz->my_flags, fz->err};
+  }
   k_u8_2d<<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
   return cudaGetLastError();
 }

@@ -500,7 +500,11 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.nunits = (int)units;
   const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
   Fin fin{};
-  if (fz) fin = Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+  if (fz) {
+    fin = Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+    fin.x = u8fin::Xchg{fz->world, fz->rank, fz->epoch, fz->slots, fz->flags, fz->my_slots,
+                        fz->my_flags, fz->err};
+  }
   if (chg)
     k_u8_3d<true><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist, fin);
   else

@@ -179,3 +179,18 @@ def test_sharded_host_streaming(ctx, world):
     with pytest.raises(eb.EccError, match="host buffer holds"):
         ctx.accumulate_host(np.zeros((5, 40, 48), np.uint8), 10, eb.Dims(45, 40, 48), [10, 15],
                             torch.zeros(512, dtype=torch.int64, device="cuda"))
+
+
+def test_fused_rank_exchange_two_processes():
+    """ecc_curve_sharded across 2 processes (torchrun; CUDA IPC between them,
+    on one GPU here, one GPU per rank in production): the histogram exchange
+    fused into the launch gives every rank the oracle's curve, 3 volumes x 3
+    consecutive steps (both exchange parities)."""
+    import subprocess
+    import sys as _sys
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    r = subprocess.run([_sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29477",
+                        __import__("os").path.join(root, "tools", "xchg_check.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert "XCHG OK 2 ranks" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
