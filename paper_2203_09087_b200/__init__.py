@@ -416,6 +416,9 @@ def _is_torch_cuda(x) -> bool:
 _live = weakref.WeakSet()
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
+
+
 class Context:
     """One ecc_ctx (one GPU, its streams and scratch)."""
 
@@ -424,6 +427,18 @@ class Context:
         _check(lib().ecc_ctx_create(int(device), C.byref(self._p)))
         self.device = device
         _live.add(self)
+
+    def _s(self, stream):
+        """The CUDA stream a device-tensor call runs on: the caller's, else
+        torch's current stream on this device, so the call is ordered with
+        the torch work that produced / consumes its tensors."""
+        if stream:
+            return stream
+        import torch
+        h = torch.cuda.current_stream(self.device).cuda_stream
+        # torch's default stream has handle 0, which the C ABI reads as "the
+        # context's stream": name the legacy default stream explicitly
+        return h if h else _CUDA_STREAM_LEGACY
 
     def close(self):
         if self._p:
@@ -615,11 +630,15 @@ class Context:
         `planes` (numpy or a CPU torch tensor; pinned memory streams at full
         PCIe speed), accumulated chunk by chunk into the device int64
         histogram `hist` (torch, 2*nbins, not zeroed here)."""
+        import torch
         if not isinstance(planes, np.ndarray):
             planes = planes.numpy()
         planes = np.ascontiguousarray(planes)
         dt = _DT[planes.dtype]
         b = (_u64 * len(bounds))(*[int(x) for x in bounds])
+        # the call runs on the context's streams and returns when done: the
+        # torch work that produced `hist` (e.g. its zero-fill) must be done
+        torch.cuda.current_stream(self.device).synchronize()
         bm = _binmap(dt, binmap)
         _check(lib().ecc_accumulate_host(self._p, planes.ctypes.data, plane0, planes.shape[0], dt,
                                          _Dims(dims.w0, dims.w1, dims.w2), b, len(bounds) - 1,
@@ -634,7 +653,7 @@ class Context:
         bm = _binmap(dt, binmap)
         _check(lib().ecc_accumulate_slab(self._p, planes.data_ptr(), dt,
                                          _Dims(dims.w0, dims.w1, dims.w2), plane0, nplanes, own0,
-                                         own1, C.byref(bm), hist.data_ptr(), stream or None))
+                                         own1, C.byref(bm), hist.data_ptr(), self._s(stream)))
 
     def compute_changes(self, planes, dims: Dims, plane0: int, own0: int, own1: int, out,
                         stream: int = 0):
@@ -643,7 +662,7 @@ class Context:
         nplanes = planes.numel() // (dims.w1 * dims.w2)
         _check(lib().ecc_compute_changes(self._p, planes.data_ptr(), dt,
                                          _Dims(dims.w0, dims.w1, dims.w2), plane0, nplanes, own0,
-                                         own1, out.data_ptr(), stream or None))
+                                         own1, out.data_ptr(), self._s(stream)))
 
     def curve_device(self, image, dims: Dims, bins, changes, chi, count, binmap=None,
                      stream: int = 0):
@@ -654,7 +673,7 @@ class Context:
         bm = _binmap(dt, binmap)
         _check(lib().ecc_curve_device(self._p, image.data_ptr(), dt, _Dims(dims.w0, dims.w1, dims.w2),
                                       C.byref(bm), bins.data_ptr(), changes.data_ptr(),
-                                      chi.data_ptr(), count.data_ptr(), stream or None))
+                                      chi.data_ptr(), count.data_ptr(), self._s(stream)))
 
     def curve_sharded(self, xchg: "Exchange", planes, dims: Dims, plane0: int, own0: int,
                       own1: int, bins, changes, chi, count, stream: int = 0):
@@ -664,12 +683,12 @@ class Context:
         _check(lib().ecc_curve_sharded(self._p, xchg._p, planes.data_ptr(),
                                        _Dims(dims.w0, dims.w1, dims.w2), plane0, nplanes, own0,
                                        own1, bins.data_ptr(), changes.data_ptr(), chi.data_ptr(),
-                                       count.data_ptr(), stream or None))
+                                       count.data_ptr(), self._s(stream)))
 
     def finalize(self, hist, nbins: int, bins, changes, chi, count, stream: int = 0):
         _check(lib().ecc_finalize(self._p, hist.data_ptr(), nbins, bins.data_ptr(),
                                   changes.data_ptr(), chi.data_ptr(), count.data_ptr(),
-                                  stream or None))
+                                  self._s(stream)))
 
     def batch2d(self, images, chi=None, presence=None, stream: int = 0):
         """Dense per-image curves for a (count, h, w) stack: chi (count, nbins)
@@ -684,7 +703,7 @@ class Context:
             if presence is None:
                 presence = torch.empty((count, nb // 32), dtype=torch.int32, device=images.device)
             _check(lib().ecc_batch2d(self._p, images.data_ptr(), 1, dt, count, h, w,
-                                     chi.data_ptr(), presence.data_ptr(), stream or None))
+                                     chi.data_ptr(), presence.data_ptr(), self._s(stream)))
             return chi, presence
         images = np.ascontiguousarray(images)
         dt = _DT[images.dtype]
@@ -699,7 +718,7 @@ class Context:
     def uniform_noise(self, tensor, seed: int = 0, stream: int = 0):
         """uniform_noise (datagen.hpp:57-62) into a device float32 tensor."""
         _check(lib().ecc_uniform_noise(self._p, tensor.data_ptr(), tensor.numel(), seed,
-                                       stream or None))
+                                       self._s(stream)))
         return tensor
 
     def gaussian_smooth(self, tensor, sigma: float, width: int, out=None, stream: int = 0):
@@ -710,7 +729,7 @@ class Context:
             out = torch.empty_like(tensor)
         _check(lib().ecc_gaussian_smooth(self._p, tensor.data_ptr(), out.data_ptr(),
                                          _dims_of(tuple(tensor.shape)), sigma, width,
-                                         stream or None))
+                                         self._s(stream)))
         return out
 
     def bench_run(self, dims: Dims, iterations: int, seed: int = 1, sigma: float = 2.0,
@@ -748,16 +767,16 @@ class Context:
         if out is None:
             out = torch.empty_like(presence)
         _check(lib().ecc_batch_zero_crossings(self._p, chi.data_ptr(), presence.data_ptr(),
-                                              chi.shape[0], dt, out.data_ptr(), stream or None))
+                                              chi.shape[0], dt, out.data_ptr(), self._s(stream)))
         return out
 
     def fill_synthetic(self, tensor, seed: int = 1, base: int = 0, stream: int = 0):
         import torch
         dt = {torch.uint8: ECC_U8, torch.uint16: ECC_U16, torch.float32: ECC_F32}[tensor.dtype]
         _check(lib().ecc_fill_synthetic(self._p, tensor.data_ptr(), dt, tensor.numel(), seed, base,
-                                        stream or None))
-        if not stream:  # on the context's own stream: make it visible to torch's streams
-            torch.cuda.ExternalStream(self.stream, device=tensor.device).synchronize()
+                                        self._s(stream)))
+        if not stream:  # a setup utility: done when it returns, visible to every stream
+            torch.cuda.current_stream(self.device).synchronize()
 
 
 _default_ctx = {}
