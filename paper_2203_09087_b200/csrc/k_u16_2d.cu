@@ -36,7 +36,7 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 struct Geom {
   const uint16_t* base;  // row plane0 of the slab
   long long pitch;       // elements between rows (multiple of 8)
-  int W0, W1, plane0, own0, P, nchunks, nstrips, band, nunits;
+  int W0, W1, plane0, nheld, own0, P, nchunks, nstrips, band, nunits;
   uint32_t nbins;
 };
 
@@ -106,7 +106,9 @@ __global__ void __launch_bounds__(NT, 1)
     const int nq = chunk_in ? min(4, (g.W1 - lo + 7) / 8) : 0;  // 16-byte groups holding pixels
 
     auto load_row = [&](int i, uint32_t (&W)[16]) {
-      if (i < 0 || i >= g.W0 || !chunk_in) {
+      // rows outside the image are collar; rows outside the held range are
+      // only the prefetch past a band's halo row (never used)
+      if (i < 0 || i >= g.W0 || i < g.plane0 || i >= g.plane0 + g.nheld || !chunk_in) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) W[j] = FULL;
         return;
@@ -241,6 +243,7 @@ cudaError_t launch_u16_2d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   g.W0 = (int)s.w0;
   g.W1 = (int)s.w1;
   g.plane0 = (int)s.plane0;
+  g.nheld = (int)s.nplanes;
   g.own0 = (int)s.own0;
   g.P = (int)(s.own1 - s.own0);
   g.nchunks = (g.W1 + 31) / 32;

@@ -55,6 +55,7 @@ struct Geom {
   long long pitch;      // bytes between rows (multiple of 16)
   int W0, W1;           // image rows, pixels per row
   int plane0;           // image row held at base
+  int nheld;            // rows held from plane0 (a streamed slab holds only its halo'd range)
   int own0, P;          // first owned row, owned rows
   int nchunks;          // 32-pixel chunks per row
   int nstrips;          // warps across a row
@@ -110,7 +111,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     const bool hi_in = lo + 16 < g.W1;  // the chunk's second 16 bytes hold image pixels
 
     auto load_row = [&](int i, uint32_t (&W)[8]) {
-      if (i < 0 || i >= g.W0 || !chunk_in) {
+      // rows outside the image are collar; rows outside the held range are
+      // only the prefetch past a band's halo row (never used)
+      if (i < 0 || i >= g.W0 || i < g.plane0 || i >= g.plane0 + g.nheld || !chunk_in) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) W[j] = FULL;
         return;
@@ -227,6 +230,7 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   g.W0 = (int)s.w0;
   g.W1 = (int)s.w1;
   g.plane0 = (int)s.plane0;
+  g.nheld = (int)s.nplanes;
   g.own0 = (int)s.own0;
   g.P = (int)(s.own1 - s.own0);
   g.nchunks = (g.W1 + 31) / 32;
