@@ -21,6 +21,7 @@
 // product).  inner == 1: row tiles of 1024 outputs; inner > 1: tiles of 32
 // coalesced inner positions x 64 outputs along the axis.
 #include <cstdint>
+#include <type_traits>
 
 #include "ecc_common.cuh"
 #include "internal.h"
@@ -105,6 +106,25 @@ __global__ void __launch_bounds__(ROW_T)
 // axis; thread (c, g) owns column c, outputs g + COL_G j.
 constexpr int COL_W = 32, COL_G = 8, COL_J = 8, COL_OUT = COL_G * COL_J;
 
+// Register-blocked taps for a compile-time width W: the thread's COL_J
+// consecutive outputs share one window of COL_J + W - 1 inputs held in
+// registers, so a tap costs a DMUL + DADD and no shared-memory load.  The
+// accumulation order per output (taps k = 0 .. W-1) is the reference's.
+template <int W, int STRIDE>
+__device__ __forceinline__ void taps_blocked(const double* xs, const double* ws, int first, int c,
+                                            double (&acc)[COL_J]) {
+  double x[COL_J + W - 1], wr[W];
+#pragma unroll
+  for (int m = 0; m < COL_J + W - 1; ++m) x[m] = xs[(first + m) * STRIDE + c];
+#pragma unroll
+  for (int k = 0; k < W; ++k) wr[k] = ws[k];
+#pragma unroll
+  for (int k = 0; k < W; ++k)
+#pragma unroll
+    for (int j = 0; j < COL_J; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn(wr[k], x[j + k]));
+}
+
+template <int W>
 __global__ void __launch_bounds__(COL_W * COL_G)
     k_smooth_cols(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
                   uint64_t inner, uint32_t ctiles, const double* __restrict__ w, int width) {
@@ -119,19 +139,21 @@ __global__ void __launch_bounds__(COL_W * COL_G)
   const int c = threadIdx.x & (COL_W - 1), g = threadIdx.x / COL_W;
   const bool col_in = c0 + c < inner;
   for (int k = threadIdx.x; k < width; k += COL_W * COL_G) ws[k] = w[k];
-  // staging: eight loads in flight per thread before any conversion
+  // staging: the whole tile's loads in flight per thread (one latency per
+  // tile) before any conversion; compile-time widths know the count
   const int nr = COL_OUT + width - 1;
-  for (int r0 = g; r0 < nr; r0 += 8 * COL_G) {
-    float v[8];
+  constexpr int NL = W > 0 ? (COL_OUT + W - 1 + COL_G - 1) / COL_G : 8;
+  for (int r0 = g; r0 < nr; r0 += NL * COL_G) {
+    float v[NL];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NL; ++u) {
       const int r = r0 + u * COL_G;
       int64_t q = p0 - half + r;
       q = q < 0 ? 0 : (q > (int64_t)L - 1 ? (int64_t)L - 1 : q);
       v[u] = (col_in && r < nr) ? __ldg(src + (uint64_t)q * inner + c0 + c) : 0.0f;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < NL; ++u) {
       const int r = r0 + u * COL_G;
       if (r < nr) xs[r * COL_W + c] = (double)v[u];
     }
@@ -140,17 +162,21 @@ __global__ void __launch_bounds__(COL_W * COL_G)
   double acc[COL_J];
 #pragma unroll
   for (int j = 0; j < COL_J; ++j) acc[j] = 0.0;
-  for (int k = 0; k < width; ++k) {
-    const double wk = ws[k];
+  if constexpr (W > 0) {
+    taps_blocked<W, COL_W>(xs, ws, g * COL_J, c, acc);  // outputs g COL_J + j
+  } else {
+    for (int k = 0; k < width; ++k) {                    // outputs g + COL_G j
+      const double wk = ws[k];
 #pragma unroll
-    for (int j = 0; j < COL_J; ++j)
-      acc[j] = __dadd_rn(acc[j], __dmul_rn(wk, xs[(g + COL_G * j + k) * COL_W + c]));
+      for (int j = 0; j < COL_J; ++j)
+        acc[j] = __dadd_rn(acc[j], __dmul_rn(wk, xs[(g + COL_G * j + k) * COL_W + c]));
+    }
   }
   if (!col_in) return;
   float* dst = out + outer * L * inner + c0 + c;
 #pragma unroll
   for (int j = 0; j < COL_J; ++j) {
-    const int64_t p = p0 + g + COL_G * j;
+    const int64_t p = p0 + (W > 0 ? g * COL_J + j : g + COL_G * j);
     if (p < (int64_t)L) dst[(uint64_t)p * inner] = __double2float_rn(acc[j]);
   }
 }
@@ -174,6 +200,31 @@ cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint6
   for (int a = 0; a < axis; ++a) outer *= ext[a];
   for (int a = axis + 1; a < 3; ++a) inner *= ext[a];
   if (L > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  // compile-time widths get the register-blocked kernels
+  auto blocked = [&](auto wc) -> bool {
+    constexpr int W = decltype(wc)::value;
+    if (width != W) return false;
+    if (inner == 1) {
+      // the contiguous axis keeps the plain row tiles: a transposed-tile
+      // register-blocked variant measured slower (826 vs 794 us at 512^3)
+      return false;
+    } else {
+      const uint64_t ctiles = (inner + COL_W - 1) / COL_W;
+      const uint64_t ptiles = (L + COL_OUT - 1) / COL_OUT;
+      if (outer * ctiles > 0x7FFFFFFFull || ptiles > 65535) return false;
+      const size_t smem = (size_t)(width + (COL_OUT + width - 1) * COL_W) * 8;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_smooth_cols<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_smooth_cols<W><<<dim3((unsigned)(outer * ctiles), (unsigned)ptiles), COL_W * COL_G, smem,
+                         st>>>(in, out, (uint32_t)L, inner, (uint32_t)ctiles, d_weights, width);
+    }
+    return true;
+  };
+  using std::integral_constant;
+  if (blocked(integral_constant<int, 5>{}) || blocked(integral_constant<int, 7>{}) ||
+      blocked(integral_constant<int, 9>{}) || blocked(integral_constant<int, 13>{}) ||
+      blocked(integral_constant<int, 25>{}))
+    return cudaGetLastError();
   if (inner == 1) {
     const int J = L <= 256 ? 1 : (L <= 512 ? 2 : 4);
     const uint64_t tiles = (L + (uint64_t)ROW_T * J - 1) / ((uint64_t)ROW_T * J);
@@ -197,8 +248,8 @@ cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint6
     if (outer * ctiles > 0x7FFFFFFFull || ptiles > 65535) return cudaErrorInvalidValue;
     const size_t smem = (size_t)(width + (COL_OUT + width - 1) * COL_W) * 8;
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_smooth_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_smooth_cols<<<dim3((unsigned)(outer * ctiles), (unsigned)ptiles), COL_W * COL_G, smem, st>>>(
+      cudaFuncSetAttribute(k_smooth_cols<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_smooth_cols<0><<<dim3((unsigned)(outer * ctiles), (unsigned)ptiles), COL_W * COL_G, smem, st>>>(
         in, out, (uint32_t)L, inner, (uint32_t)ctiles, d_weights, width);
   }
   return cudaGetLastError();
