@@ -189,8 +189,12 @@ def test_fused_rank_exchange_two_processes():
     import subprocess
     import sys as _sys
     root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    import socket
+    with socket.socket() as so:  # a free port for the rendezvous
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
     r = subprocess.run([_sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29477",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
                         __import__("os").path.join(root, "tools", "xchg_check.py")],
                        capture_output=True, text=True, timeout=300)
     assert "XCHG OK 2 ranks" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
