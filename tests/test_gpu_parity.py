@@ -427,3 +427,15 @@ def test_f32_sorted_2d_infinities_and_signed_zeros(ctx):
         assert _same(a.values, a.changes, *oracle.vcec(img)), shape
         if oracle.ref_available():
             assert _same(a.values, a.changes, *oracle.ref_vcec(img)), shape
+
+
+def test_randomised_differential_smoke():
+    """tools/fuzz.py for 15 s: random dtype / shape / value range / public
+    path against the oracle (a 240 s run: profiles/r01m_fuzz.json)."""
+    import subprocess
+    import sys as _sys
+    import os as _os
+    root = _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    r = subprocess.run([_sys.executable, _os.path.join(root, "tools", "fuzz.py"), "15", "7"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and " 0 failures" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
