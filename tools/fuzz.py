@@ -60,8 +60,16 @@ def rand_image(rng, shape):
 
 
 def run_path(ctx, rng, img, bm):
-    path = rng.choice(["host", "device", "plan", "sharded", "curve_device"])
+    path = rng.choice(["host", "device", "plan", "sharded", "curve_device", "batch2d"])
     dims = eb.Dims.of(img.shape)
+    if path == "batch2d" and img.ndim == 2 and img.dtype != np.float32:
+        chi, pres = ctx.batch2d(img[None])
+        t, cc = eb.curve_batch_to_points(chi[0], pres[0].view(np.uint32))
+        ch = np.diff(np.concatenate([[0], cc]))
+        return path, eb.GlobalVcec(t.astype(img.dtype), ch)
+    if path == "batch2d":
+        path = "host"
+        return path, ctx.vcec(img, binmap=bm)
     if path == "host":
         return path, ctx.vcec(img, binmap=bm)
     if path == "device":
