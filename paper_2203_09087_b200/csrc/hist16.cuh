@@ -2,17 +2,20 @@
 // 16-bit kernels (k_u16_3d.cu, k_batch16.cu).
 //
 // Bin k's running change sum lives in half (k & 1) of word k >> 1, biased
-// by 32768.  A half is "in band" while its biased value lies in
-// [16384, 49151] (bit 15 XOR bit 14 of the half set).  Every update is an
-// atomic add that returns the old word; an update that changes the band of
-// its half (either direction) hands exactly the value it saw to the caller's
-// spill target and subtracts it from the half, so (half + spills) is always
-// the exact sum and halves stay far from the carry boundary: a half would
-// need thousands more updates of the same bin between the crossing atomic
-// and the fix a few instructions later to wrap.  Updates are issued in
-// groups so their atomic latencies overlap; one warp vote per group decides
-// whether any lane has a fix to make (rare), and the fix itself is
-// predicated, so the common path has no divergent branches.
+// by 32768.  A half is "in band" while its unbiased value lies in
+// [-8192, 8191] (biased bits 15..13 = 011 or 100).  Every update is an
+// atomic add that returns the old word; an update that leaves its half out
+// of band moves the half's whole current value to the caller's spill target
+// with a compare-and-swap on the word (retried while other updates race it,
+// and dropped once the half is back in band), so (half + spills) is always
+// the exact sum and a half is reset to exactly 0 -- never over-corrected, so
+// it stays tens of thousands of updates away from the 16-bit wrap however
+// hot the bin (an earlier version subtracted the value each crossing thread
+// had seen, and several crossings racing on one bin of a 2-valued image
+// could push the half past the wrap; tests/test_gpu_parity.py now covers
+// that).  Updates are issued in groups so their atomic latencies overlap;
+// one warp vote per group decides whether any lane has a fix to make
+// (rare), and the common path has no divergent branches.
 #pragma once
 #include <cstdint>
 
@@ -39,24 +42,41 @@ __device__ __forceinline__ void issue(uint32_t hbase, uint32_t key, uint32_t chu
                : "memory");
 }
 
-// Band change of the updated half.  Only that half can differ between the
-// old and new word (the band keeps the low half from carrying into the high
-// one), so one constant mask covers both halves.
+// Nonzero when the updated half is out of band after this update.  Only
+// that half can differ between the old and the new word (the band keeps the
+// low half from carrying into the high one); the mask restricts the test to
+// it.  In band: biased bits 15..13 = 011 or 100, i.e. t = w ^ (w << 1) has
+// bit 15 set and bit 14 clear.
 __device__ __forceinline__ uint32_t crossed(const Upd& u) {
-  const uint32_t d = u.old ^ (u.old + u.add);
-  return (d ^ (d << 1)) & 0x80008000u;
+  const uint32_t w = u.old + u.add;
+  const uint32_t t = w ^ (w << 1);
+  const uint32_t half = __funnelshift_l(0u, 0xC000u, u.key << 4);  // this half's bits 15..14
+  return ((~t & 0x80008000u) | (t & 0x40004000u)) & half;
 }
 
-// the rare fix: predicated shared add of -after, and `spill(key, after)`
+// the rare fix: move the half's current value to `spill(key, value)` with a
+// compare-and-swap that leaves the half at exactly 0 (biased 32768)
 template <class Spill>
 __device__ __forceinline__ void fix(uint32_t hbase, const Upd& u, uint32_t cross, Spill& spill) {
   if (cross) {
+    const uint32_t addr = hbase + (u.key >> 1) * 4u;
     const uint32_t sh = (u.key & 1u) << 4;
-    const int after = (int)(((u.old + u.add) >> sh) & 0xFFFFu) - 32768;
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(hbase + (u.key >> 1) * 4u),
-                 "r"((uint32_t)(-after) << sh)
-                 : "memory");
-    spill(u.key, after);
+    uint32_t cur = u.old + u.add;
+    for (;;) {
+      const int h = (int)((cur >> sh) & 0xFFFFu) - 32768;
+      if (h >= -8192 && h < 8192) break;  // back in band: another update moved it
+      const uint32_t want = cur - ((uint32_t)h << sh);
+      uint32_t prev;
+      asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;"
+                   : "=r"(prev)
+                   : "r"(addr), "r"(cur), "r"(want)
+                   : "memory");
+      if (prev == cur) {
+        spill(u.key, h);
+        break;
+      }
+      cur = prev;
+    }
   }
 }
 

@@ -19,6 +19,7 @@
 #include <cub/cub.cuh>
 
 #include "ecc_common.cuh"
+#include "hist16.cuh"
 #include "internal.h"
 
 namespace eccb {
@@ -26,13 +27,6 @@ namespace eccb {
 namespace {
 
 constexpr int NT = 1024;
-
-__device__ __forceinline__ int sext16(uint32_t v) { return (int)(int16_t)(v & 0xFFFF); }
-
-__device__ __forceinline__ int half_of(uint32_t word, bool hi) {
-  const int lo = sext16(word);
-  return hi ? (int)((int32_t)(word - (uint32_t)lo) >> 16) : lo;
-}
 
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
@@ -62,8 +56,10 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* pres = sm + nwords;
   uint32_t* spilled = pres + nbins / 32;  // PACKED only
   const uint32_t nsm = nwords + nbins / 32 + (PACKED ? nbins / 32 : 0);
-  for (uint32_t q = threadIdx.x; q < nsm; q += NT) sm[q] = 0;
+  for (uint32_t q = threadIdx.x; q < nsm; q += NT)
+    sm[q] = (PACKED && q < nwords) ? hist16::BIAS : 0u;  // packed halves start at the bias
   __syncthreads();
+  const uint32_t hbase = static_cast<uint32_t>(__cvta_generic_to_shared(bins));
   const T* img = data + (size_t)blockIdx.x * h * w;
   int32_t* row = chi + (size_t)blockIdx.x * nbins;
   uint32_t* pres_row = presence + (size_t)blockIdx.x * (nbins / 32);
@@ -109,18 +105,15 @@ __global__ void __launch_bounds__(NT, 1)
       if (!((pres[v >> 5] >> (v & 31)) & 1u)) atomicOr(&pres[v >> 5], 1u << (v & 31));
       if (ch != 0) {
         if constexpr (PACKED) {
-          const uint32_t q = v >> 1;
-          const bool hi = v & 1;
-          const uint32_t add = hi ? ((uint32_t)ch << 16) : (uint32_t)ch;
-          const uint32_t old = atomicAdd(&bins[q], add);
-          const int before = half_of(old, hi), after = half_of(old + add, hi);
-          const bool in_b = before >= -16384 && before <= 16383;
-          const bool in_a = after >= -16384 && after <= 16383;
-          if (in_b && !in_a) {
-            atomicAdd(&bins[q], hi ? (uint32_t)(-after) << 16 : (uint32_t)(-after));
-            atomicAdd(&scratch[v], after);
-            atomicOr(&spilled[v >> 5], 1u << (v & 31));
-          }
+          // the packed table of hist16.cuh: exact out-of-band moves to the
+          // per-SM scratch row
+          hist16::Upd u;
+          hist16::issue(hbase, v, (uint32_t)ch, u);  // 32-bit two's complement (no borrow: biased)
+          auto spill = [&](uint32_t key, int val) {
+            atomicAdd(&scratch[key], val);
+            atomicOr(&spilled[key >> 5], 1u << (key & 31));
+          };
+          hist16::fix(hbase, u, hist16::crossed(u), spill);
         } else {
           atomicAdd(&bins[v], (uint32_t)ch);
         }
@@ -138,7 +131,7 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
   auto bin_sum = [&](uint32_t b) -> int {
     if constexpr (PACKED) {
-      int s = half_of(bins[b >> 1], b & 1);
+      int s = (int)((bins[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
       if ((spilled[b >> 5] >> (b & 31)) & 1u) s += scratch[b];
       return s;
     } else {

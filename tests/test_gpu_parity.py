@@ -439,3 +439,19 @@ def test_randomised_differential_smoke():
     r = subprocess.run([_sys.executable, _os.path.join(root, "tools", "fuzz.py"), "15", "7"],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and " 0 failures" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("lo,hi", [(0, 2), (7, 9), (65530, 65536), (1000, 1006)])
+@pytest.mark.parametrize("shape", [(2000, 512), (2000, 1024), (2035, 1197), (1200, 300)])
+def test_hot_bins_packed_histogram(ctx, lo, hi, shape):
+    """Images with only a few distinct values: one CTA accumulates per-bin
+    sums far beyond the 16-bit halves of the packed 65536-bin table (both
+    batched kernels); the exact compare-and-swap spill keeps them exact."""
+    rng = np.random.default_rng(lo + shape[1])
+    img = rng.integers(lo, hi, shape).astype(np.uint16)
+    chi, pres = ctx.batch2d(img[None])
+    t, cc = eb.curve_batch_to_points(chi[0], pres[0].view(np.uint32))
+    v, c = oracle.vcec(img)
+    assert np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
+    a = ctx.vcec(img)
+    assert np.array_equal(a.changes, c)

@@ -6,7 +6,7 @@ extremes), random path (host / device whole volume, chunked plan, host DMA,
 sharded slabs, fused device curve).  Prints one line per failure and a
 summary; exits non-zero on any mismatch.
 
-  python tools/fuzz.py [seconds] [seed]
+  python tools/fuzz.py [seconds] [seed] [large]
 """
 import os
 import sys
@@ -29,7 +29,14 @@ def grid_values(bm, k):
             np.float64(np.float32(bm["step"]))).astype(np.float32)
 
 
+LARGE = False
+
+
 def rand_shape(rng):
+    if LARGE:
+        if rng.random() < 0.4:
+            return (int(rng.integers(100, 3000)), int(rng.integers(900, 3000)))
+        return (int(rng.integers(20, 200)), int(rng.integers(30, 300)), int(rng.integers(30, 300)))
     if rng.random() < 0.4:
         w = int(rng.choice([1, 2, 31, 32, 33, 63, 64, 65, 959, 960, 961, 1000, int(rng.integers(1, 200))]))
         return (int(rng.integers(1, 70)), w)
@@ -117,8 +124,10 @@ def run_path(ctx, rng, img, bm):
 
 
 def main():
+    global LARGE
     seconds = float(sys.argv[1]) if len(sys.argv) > 1 else 120
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    LARGE = len(sys.argv) > 3 and sys.argv[3] == "large"
     rng = np.random.default_rng(seed)
     ctx = eb.context(0)
     t0, n, bad = time.time(), 0, 0
