@@ -455,3 +455,18 @@ def test_hot_bins_packed_histogram(ctx, lo, hi, shape):
     assert np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
     a = ctx.vcec(img)
     assert np.array_equal(a.changes, c)
+
+
+@pytest.mark.parametrize("shape", [(2000, 32, 40), (400, 64, 64), (200000, 32), (3000, 2000)])
+def test_hot_bins_16bit_kernels(ctx, shape):
+    """Two-valued u16 / quantised-f32 images through the 3D and single-image
+    2D 16-bit kernels (each CTA sees bins with sums far beyond 16 bits)."""
+    rng = np.random.default_rng(len(shape) + shape[0])
+    img = rng.integers(5, 7, shape).astype(np.uint16)
+    a = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(a.values.astype(np.int64), v.astype(np.int64))
+    assert np.array_equal(a.changes, c)
+    q = (img.astype(np.float64) * 2.0 ** -16).astype(np.float32)
+    b = ctx.vcec(q, binmap=eb.quantised_binmap(65536))
+    assert np.array_equal(b.changes, c)
