@@ -33,6 +33,10 @@ constexpr int NW = ECC_B16_NW;  // warps per CTA
 constexpr int NT = NW * 32;
 constexpr int HWORDS = 32768, PWORDS = 2048;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
+#ifndef ECC_HGRP
+#define ECC_HGRP 8
+#endif
+constexpr int HGRP = ECC_HGRP;  // pixels per atomic group (divides 32)
 constexpr uint32_t BIAS = 0x80008000u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -195,10 +199,10 @@ __global__ void __launch_bounds__(NT, 1)
           atomicOr(&spilled[key >> 5], 1u << (key & 31));
         };
 #pragma unroll
-        for (int g4 = 0; g4 < 32; g4 += 4) {
-          hist16::Upd u[4];
+        for (int g4 = 0; g4 < 32; g4 += HGRP) {
+          hist16::Upd u[HGRP];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < HGRP; ++j) {
             const int p = g4 + j, r = p & 7, b = p >> 3;
             const uint32_t chu =
                 bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
@@ -206,12 +210,12 @@ __global__ void __launch_bounds__(NT, 1)
             hist16::mark(pbase, key, (vmr >> p) & 1u);
             hist16::issue(hbase, key, chu, u[j]);
           }
-          uint32_t cr[4], any = 0;
+          uint32_t cr[HGRP], any = 0;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          for (int j = 0; j < HGRP; ++j) any |= (cr[j] = hist16::crossed(u[j]));
           if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) hist16::fix(hbase, u[j], cr[j], spill);
+            for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, u[j], cr[j], spill);
           }
         }
       }

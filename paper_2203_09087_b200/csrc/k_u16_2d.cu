@@ -32,6 +32,10 @@ constexpr int HWORDS = 32768, PWORDS = 2048;
 constexpr int SMEM_BYTES = (HWORDS + PWORDS) * 4;
 constexpr int STRIP = 30;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
+#ifndef ECC_HGRP
+#define ECC_HGRP 8
+#endif
+constexpr int HGRP = ECC_HGRP;  // pixels per atomic group (divides 32)
 
 struct Geom {
   const uint16_t* base;  // row plane0 of the slab
@@ -181,10 +185,10 @@ __global__ void __launch_bounds__(NT, 1)
                            d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr};
           bits::transpose8(V);
 #pragma unroll
-          for (int g4 = 0; g4 < 32; g4 += 4) {
-            hist16::Upd up[4];
+          for (int g4 = 0; g4 < 32; g4 += HGRP) {
+            hist16::Upd up[HGRP];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < HGRP; ++j) {
               const int p = g4 + j, r = p & 7, b = p >> 3;
               const uint32_t chu =
                   bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
@@ -192,12 +196,12 @@ __global__ void __launch_bounds__(NT, 1)
               hist16::mark(pbase, key, (vmr >> p) & 1u);
               hist16::issue(hbase, key, chu, up[j]);
             }
-            uint32_t cr[4], any = 0;
+            uint32_t cr[HGRP], any = 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) any |= (cr[j] = hist16::crossed(up[j]));
+            for (int j = 0; j < HGRP; ++j) any |= (cr[j] = hist16::crossed(up[j]));
             if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-              for (int j = 0; j < 4; ++j) hist16::fix(hbase, up[j], cr[j], spill);
+              for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, up[j], cr[j], spill);
             }
           }
         }

@@ -50,6 +50,10 @@ constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + (HWORDS + PWORDS + 1) * 4;  // + set-bit count
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr uint32_t BIAS = 0x80008000u;  // both halves at 32768
+#ifndef ECC_U16_GRP
+#define ECC_U16_GRP 15
+#endif
+constexpr int GRP = ECC_U16_GRP;  // voxels per atomic group (divides 30)
 
 struct Geom {
   int W0, W1, W2, plane0, own0, P, Gy, Gz, ncols, seglen, nunits;
@@ -300,10 +304,10 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
         // groups of voxels: atomic latencies overlap, one vote per group for
         // the rare out-of-band fix (hist16.cuh)
 #pragma unroll
-        for (int g5 = 1; g5 <= 30; g5 += 5) {
-          hist16::Upd u[5];
+        for (int g5 = 1; g5 <= 30; g5 += GRP) {
+          hist16::Upd u[GRP];
 #pragma unroll
-          for (int j = 0; j < 5; ++j) {
+          for (int j = 0; j < GRP; ++j) {
             const int p = g5 + j, r = p & 7, b = p >> 3;
             const uint32_t chu =
                 bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
@@ -330,12 +334,12 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
             }
             hist16::issue(hbase, key, chu, u[j]);
           }
-          uint32_t cr[5], any = 0;
+          uint32_t cr[GRP], any = 0;
 #pragma unroll
-          for (int j = 0; j < 5; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          for (int j = 0; j < GRP; ++j) any |= (cr[j] = hist16::crossed(u[j]));
           if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-            for (int j = 0; j < 5; ++j) hist16::fix(hbase, u[j], cr[j], spill);
+            for (int j = 0; j < GRP; ++j) hist16::fix(hbase, u[j], cr[j], spill);
           }
         }
       };
