@@ -50,6 +50,9 @@ constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + (HWORDS + PWORDS + 1) * 4;  // + set-bit count
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr uint32_t BIAS = 0x80008000u;  // both halves at 32768
+#ifndef ECC_AFF_U
+#define ECC_AFF_U 8
+#endif
 #ifndef ECC_U16_GRP
 #define ECC_U16_GRP 15
 #endif
@@ -428,12 +431,13 @@ __global__ void k_affine_keys(const float* __restrict__ v, uint64_t rows, uint32
   const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   if (pitch == w2 && (w2 & 3) == 0) {
-    // contiguous rows: a flat grid-stride over float4 groups, four loads in
-    // flight per thread (HBM needs ~40 KB in flight per SM)
+    // contiguous rows: a flat grid-stride over float4 groups, ECC_AFF_U (8)
+    // loads in flight per thread (measured 1.08 ms at 8, 1.14 at 4, 1.30 at 2
+    // for C4's 4.3 GB read + 2.1 GB written: 90 % of HBM)
     const uint64_t n4 = rows * w2 / 4;
     const float4* src = reinterpret_cast<const float4*>(v);
     uint2* dst = reinterpret_cast<uint2*>(keys);
-    constexpr int U = 4;
+    constexpr int U = ECC_AFF_U;
     uint64_t i = tid;
     for (; i + (U - 1) * nthreads < n4; i += U * nthreads) {
       float4 x[U];
