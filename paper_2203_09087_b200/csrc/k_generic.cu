@@ -279,14 +279,35 @@ cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sm
 __global__ void k_key_range(const float* __restrict__ v, uint64_t n, uint32_t* flags,
                             uint32_t* mm) {
   uint32_t lo = 0xFFFFFFFFu, hi = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const float x = __ldg(v + i);
-    if (x != x) atomicOr(flags, kFlagNaN);
+  bool nan = false;
+  auto take = [&](float x) {
+    nan |= x != x;
     const uint32_t k = float_order_key_bits(__float_as_uint(x));
     lo = min(lo, k);
     hi = max(hi, k);
+  };
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(v) & 15) == 0;
+  const uint64_t n4 = vec ? n / 4 : 0;
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  // float4 groups, four loads in flight per thread
+  uint64_t i = tid;
+  for (; i + 3 * nt < n4; i += 4 * nt) {
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldcs(v4 + i + u * nt);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      take(x[u].x); take(x[u].y); take(x[u].z); take(x[u].w);
+    }
   }
+  for (; i < n4; i += nt) {
+    const float4 x = __ldcs(v4 + i);
+    take(x.x); take(x.y); take(x.z); take(x.w);
+  }
+  for (uint64_t j = 4 * n4 + tid; j < n; j += nt) take(__ldg(v + j));
+  if (nan) atomicOr(flags, kFlagNaN);
   lo = __reduce_min_sync(0xFFFFFFFFu, lo);
   hi = __reduce_max_sync(0xFFFFFFFFu, hi);
   if ((threadIdx.x & 31) == 0) {
@@ -302,9 +323,27 @@ __global__ void k_key_range(const float* __restrict__ v, uint64_t n, uint32_t* f
 __global__ void k_order_keys(const float* __restrict__ v, uint64_t n,
                              uint32_t* __restrict__ keys, const uint32_t* mm) {
   const uint32_t lo = mm[0];
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    keys[i] = float_order_key_bits(__float_as_uint(v[i])) - lo;
+  const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(keys)) & 15) == 0;
+  const uint64_t n4 = vec ? n / 4 : 0;
+  auto key = [&](float x) { return float_order_key_bits(__float_as_uint(x)) - lo; };
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  uint4* k4 = reinterpret_cast<uint4*>(keys);
+  uint64_t i = tid;
+  for (; i + 3 * nt < n4; i += 4 * nt) {
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = __ldcs(v4 + i + u * nt);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      k4[i + u * nt] = make_uint4(key(x[u].x), key(x[u].y), key(x[u].z), key(x[u].w));
+  }
+  for (; i < n4; i += nt) {
+    const float4 x = __ldcs(v4 + i);
+    k4[i] = make_uint4(key(x.x), key(x.y), key(x.z), key(x.w));
+  }
+  for (uint64_t j = 4 * n4 + tid; j < n; j += nt) keys[j] = key(__ldg(v + j));
 }
 
 __global__ void k_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm) {
