@@ -628,6 +628,58 @@ void write_values(ecc_dtype dtype, bool sorted, const AffineMap& am, const BinRe
   }
 }
 
+// General f32 over a whole resident volume when its order keys span fewer
+// than 2^24 values (e.g. smoothed fields): a dense histogram indexed by
+// (order key - min key) replaces the radix sort + reduce-by-key -- the
+// generic stencil's HIST mode adds each voxel's change and count to its
+// key's bin with global int64 atomics, and K3 compacts the occurring keys in
+// ascending order, which is exactly build_index_counts' (value, summed
+// change) list (value_index.hpp:159-197).  *used = false when the span is
+// too wide (the sort path runs instead).  The curve is left in the result
+// block (layout L); keys are bins + *key_lo.
+constexpr uint64_t kDenseKeySpan = 1ull << 24;
+
+int dense_sorted(ecc_ctx* ctx, const Slab& s, cudaStream_t st, ResultLayout* L, uint32_t* key_lo,
+                 bool* used) {
+  *used = false;
+  const uint64_t n64 = (uint64_t)(s.own1 - s.own0) * s.w1 * s.w2;
+  if (n64 < (1ull << 20)) return ECC_OK;  // small volumes: the sort is cheap
+  const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
+  CKI(ctx->flags.ensure(16));
+  uint32_t* mm = ctx->flags.as<uint32_t>() + 1;
+  const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+  CKR(cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, st));
+  CKR(launch_key_range(owned, n64, ctx->flags.as<uint32_t>(), mm, ctx->sms, st));
+  ctx->launches += 1;
+  uint32_t range[2] = {0, 0};
+  CKR(cudaMemcpyAsync(range, mm, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  CKI(read_flags(ctx, st));  // NaN
+  const uint64_t span = (uint64_t)(range[1] - range[0]) + 1;
+  if (span > kDenseKeySpan) return ECC_OK;
+  AffineMap am{};
+  am.keyed = 1;
+  am.key_lo = range[0];
+  const uint32_t nbins = (uint32_t)span;
+  CKI(ctx->hist.ensure(2 * (uint64_t)nbins * 8));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * (uint64_t)nbins * 8, st));
+  CKR(launch_generic_accumulate(s, ECC_F32, true, am, ctx->hist.as<int64_t>(), nbins,
+                                ctx->flags.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 1;
+  *L = ResultLayout(nbins);
+  CKI(ctx->res.ensure(L->bytes));  // device only: the host reads back just the m points
+  uint8_t* d = ctx->res.as<uint8_t>();
+  CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
+  CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, reinterpret_cast<uint32_t*>(d + L->bins),
+                      reinterpret_cast<int64_t*>(d + L->changes),
+                      reinterpret_cast<int64_t*>(d + L->chi), reinterpret_cast<uint64_t*>(d),
+                      ctx->finscr.p, st));
+  ctx->launches += 1;
+  *key_lo = range[0];
+  *used = true;
+  return ECC_OK;
+}
+
 // Whole device-resident volume -> BinResult.
 int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
                const ecc_binmap* bm, cudaStream_t st, BinResult* res, bool* sorted_out,
@@ -642,6 +694,28 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
   CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
   const Slab s = make_slab(d_data, dims, 0, dims.w0, 0, dims.w0);
   if (sorted) {
+    ResultLayout L(1);
+    uint32_t key_lo = 0;
+    bool dense = false;
+    CKI(dense_sorted(ctx, s, st, &L, &key_lo, &dense));
+    if (dense) {
+      // read the point count, then only the m compacted points
+      const uint8_t* d = ctx->res.as<uint8_t>();
+      uint64_t m = 0;
+      CKR(cudaMemcpyAsync(&m, d, 8, cudaMemcpyDeviceToHost, st));
+      CKR(cudaStreamSynchronize(st));
+      res->keys.resize(m);
+      res->changes.resize(m);
+      res->chi.resize(m);
+      if (m) {
+        CKR(cudaMemcpyAsync(res->keys.data(), d + L.bins, m * 4, cudaMemcpyDeviceToHost, st));
+        CKR(cudaMemcpyAsync(res->changes.data(), d + L.changes, m * 8, cudaMemcpyDeviceToHost, st));
+        CKR(cudaMemcpyAsync(res->chi.data(), d + L.chi, m * 8, cudaMemcpyDeviceToHost, st));
+        CKR(cudaStreamSynchronize(st));
+      }
+      for (auto& k : res->keys) k += key_lo;  // bins -> order keys
+      return ECC_OK;
+    }
     uint64_t n = 0;
     CKI(sorted_slab(ctx, s, st, dims.w0 * dims.w1 * dims.w2, &n));
     CKI(read_flags(ctx, st));
@@ -1509,6 +1583,7 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
   CKR(cudaEventCreate(&e2));
   double smooth_ms = 0, ecc_ms = 0;
   uint64_t m = 0;
+  const uint8_t* last_chi = nullptr;  // device int64 chi of the last curve
   int rc = ECC_OK;
   const Slab s = make_slab(img, dims, 0, dims.w0, 0, dims.w0);
   const auto t0 = clk::now();
@@ -1520,10 +1595,23 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
     // process_image + vcec_to_ecc (streaming.hpp:332-338, curve.hpp:28-35)
     // on the sorted f32 path; the curve stays in device memory
     cudaMemsetAsync(ctx->flags.p, 0, 4, st);
-    uint64_t nacc = 0;
-    rc = sorted_slab(ctx, s, st, n, &nacc);
-    if (rc == ECC_OK) rc = read_flags(ctx, st);
-    if (rc == ECC_OK) rc = sorted_finish(ctx, st, nacc, false, nullptr, &m);
+    // dense key histogram when the key span allows (no sort), else the sort
+    ResultLayout L(1);
+    uint32_t key_lo = 0;
+    bool dense = false;
+    rc = dense_sorted(ctx, s, st, &L, &key_lo, &dense);
+    if (rc == ECC_OK && dense) {
+      rc = cudaMemcpyAsync(&m, ctx->res.p, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess
+               ? ECC_OK
+               : fail(ECC_ECUDA, "count readback failed");
+      last_chi = ctx->res.as<uint8_t>() + L.chi;
+    } else if (rc == ECC_OK) {
+      uint64_t nacc = 0;
+      rc = sorted_slab(ctx, s, st, n, &nacc);
+      if (rc == ECC_OK) rc = read_flags(ctx, st);
+      if (rc == ECC_OK) rc = sorted_finish(ctx, st, nacc, false, nullptr, &m);
+      last_chi = ctx->chi.as<uint8_t>();
+    }
     cudaEventRecord(e2, st);
     cudaEventSynchronize(e2);
     float a = 0, b = 0;
@@ -1543,10 +1631,9 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
   rep->smooth_avg_s = smooth_ms * 1e-3 / it;
   rep->ecc_gvox_per_s = ecc_ms > 0 ? (double)n * it / (ecc_ms * 1e-3) / 1e9 : 0;
   rep->last_points = m;
-  if (m > 0) {
-    CKR(cudaMemcpy(&rep->last_chi_first, ctx->chi.p, 8, cudaMemcpyDeviceToHost));
-    CKR(cudaMemcpy(&rep->last_chi_last, ctx->chi.as<int64_t>() + (m - 1), 8,
-                   cudaMemcpyDeviceToHost));
+  if (m > 0 && last_chi) {
+    CKR(cudaMemcpy(&rep->last_chi_first, last_chi, 8, cudaMemcpyDeviceToHost));
+    CKR(cudaMemcpy(&rep->last_chi_last, last_chi + (m - 1) * 8, 8, cudaMemcpyDeviceToHost));
   }
   return ECC_OK;
 }

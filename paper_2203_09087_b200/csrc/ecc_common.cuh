@@ -108,6 +108,10 @@ struct AffineMap {
   double inv_step;
   uint32_t nbins;
   float pow2_scale;  // 1/step when lo == 0 and step is a power of two, else 0
+  // "keyed" map of the dense sorted-f32 path: bin = order key - key_lo
+  // (value_index.hpp:95-99 order, every distinct value its own bin)
+  int keyed = 0;
+  uint32_t key_lo = 0;
 };
 
 __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,

@@ -34,6 +34,8 @@ template <class T, bool AFFINE>
 __device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am,
                                            uint32_t* flags) {
   if constexpr (AFFINE) {
+    if (am.keyed)  // dense sorted-f32 path: the order key relative to the minimum
+      return float_order_key_bits(__float_as_uint(static_cast<float>(v))) - am.key_lo;
     return affine_bin(am, static_cast<float>(v), flags);
   } else {
     return static_cast<uint32_t>(v);

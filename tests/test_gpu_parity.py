@@ -470,3 +470,29 @@ def test_hot_bins_16bit_kernels(ctx, shape):
     q = (img.astype(np.float64) * 2.0 ** -16).astype(np.float32)
     b = ctx.vcec(q, binmap=eb.quantised_binmap(65536))
     assert np.array_equal(b.changes, c)
+
+
+@pytest.mark.parametrize("case", ["smoothed", "narrow", "wide", "few", "signed_zero_inf"])
+def test_f32_sorted_dense_and_sort_paths(ctx, case):
+    """General f32 volumes of >= 2^20 voxels: order-key spans < 2^24 take the
+    dense key histogram (no sort), wider spans the radix sort; both equal the
+    oracle's (value, summed change) list."""
+    rng = np.random.default_rng(hash(case) % 1000)
+    shape = (64, 128, 160)
+    if case == "smoothed":
+        img = oracle.gaussian_smooth(oracle.uniform_noise(shape, 3), 2.0, 13)
+    elif case == "narrow":
+        img = (0.75 + rng.random(shape) * 2.0 ** -8).astype(np.float32)
+    elif case == "wide":
+        img = (rng.standard_normal(shape) * 1e3).astype(np.float32)
+    elif case == "few":
+        img = rng.choice(np.array([0.1, 0.2, 0.3], np.float32), size=shape)
+    else:
+        img = rng.choice(np.array([-0.0, 0.0, 1.0, np.inf], np.float32), size=shape)
+    a = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(np.asarray(a.values, np.float32).view(np.uint32), np.asarray(v, np.float32).view(np.uint32))
+    assert np.array_equal(a.changes, c)
+    import torch
+    b = ctx.vcec(torch.from_numpy(img).cuda())
+    assert np.array_equal(b.changes, c)

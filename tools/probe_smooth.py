@@ -18,3 +18,14 @@ print("smooth 512^3 w13:", round(a.elapsed_time(b) / 5, 3), "ms", flush=True)
 for _ in range(3):
     r = ctx.bench_run(eb.Dims(512, 512, 512), 3)
     print("bench_run: smooth", round(r.smooth_avg_s * 1e3, 2), "ms, ecc", round(r.ecc_avg_s * 1e3, 2), "ms", flush=True)
+# the general-f32 curve of the smoothed volume through ecc_vcec (dense key
+# histogram when the key span allows), device time of the whole call
+import time
+y = ctx.gaussian_smooth(x, 2.0, 13)
+torch.cuda.synchronize()
+for _ in range(2): ctx.vcec(y)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(5): v = ctx.vcec(y)
+t1 = time.perf_counter()
+print("vcec smoothed 512^3 (dense path if the key span allows):", round((t1 - t0) / 5 * 1e3, 2), "ms;", v.size(), "values", flush=True)
