@@ -45,7 +45,14 @@ def rand_shape(rng):
 
 
 def rand_image(rng, shape):
-    kind = rng.choice(["u8", "u16", "f32pool", "f32affine"])
+    kind = rng.choice(["u8", "u16", "f32pool", "f32affine", "f32narrow"])
+    if kind == "f32narrow":  # general f32 with a narrow key span (the dense path)
+        base = np.float32(rng.choice([0.3, 1.0, -2.0, 1000.0]))
+        spread = float(rng.choice([2.0 ** -12, 2.0 ** -6, 1.0]))
+        img = (base + rng.random(shape) * spread).astype(np.float32)
+        if rng.random() < 0.3:
+            img = np.round(img * 64) / 64  # ties
+        return img.astype(np.float32), None
     if kind == "u8":
         lo, hi = (0, 256) if rng.random() < 0.5 else (int(rng.integers(0, 250)), 256)
         hi = min(256, lo + int(rng.integers(1, 257)))
