@@ -486,6 +486,9 @@ struct ToI64 {
   __host__ __device__ int64_t operator()(int8_t v) const { return v; }
 };
 
+// order-key spans up to this many values take the dense histogram (no sort)
+constexpr uint64_t kDenseKeySpan = 1ull << 24;
+
 // Appends the slab's reduced (order key, change sum) runs to the device
 // accumulator ctx->akeys / ctx->asums at offset *n (no host round trip).
 int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_voxels,
@@ -501,24 +504,52 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
   CKI(ctx->count.ensure(8));
   CKI(ctx->akeys.ensure(total_voxels * 4));
   CKI(ctx->asums.ensure(total_voxels * 8));
-  CKR(launch_generic_changes(s, ECC_F32, ctx->ch8.as<int8_t>(), ctx->sms, st));
   const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
-  // flags words 1, 2: min / max order key -> the bit range the sort must cover
+  // flags words 1, 2: min / max order key -> dense histogram or the bit range
+  // the sort must cover
+  CKI(ctx->flags.ensure(16));
   uint32_t* mm = ctx->flags.as<uint32_t>() + 1;
   {
     const uint32_t init[2] = {0xFFFFFFFFu, 0u};
     CKR(cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, st));
   }
   CKR(launch_key_range(owned, n64, ctx->flags.as<uint32_t>(), mm, ctx->sms, st));
-  CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), mm, ctx->sms, st));
-  ctx->launches += 3;
+  ctx->launches += 1;
   uint32_t range[2] = {0, 0};
   CKR(cudaMemcpyAsync(range, mm, 8, cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
   const uint32_t span = n64 ? range[1] - range[0] : 0;
-  const int bit0 = 0, bit1 = span ? 32 - __builtin_clz(span) : 1;
   uint32_t* out_keys = ctx->akeys.as<uint32_t>() + *n_acc;
   int64_t* out_sums = ctx->asums.as<int64_t>() + *n_acc;
+  if (n64 >= (1ull << 20) && (uint64_t)span + 1 <= kDenseKeySpan) {
+    // dense order-key histogram (see dense_sorted): K3's compaction writes
+    // the occurring (key - min, summed change) pairs straight into the run
+    // accumulator; the minimum is added back
+    const uint32_t nbins = span + 1;
+    AffineMap am{};
+    am.keyed = 1;
+    am.key_lo = range[0];
+    CKI(ctx->hist.ensure(2 * (uint64_t)nbins * 8));
+    CKI(ctx->sums.ensure((uint64_t)nbins * 8));
+    CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
+    CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * (uint64_t)nbins * 8, st));
+    CKR(launch_generic_accumulate(s, ECC_F32, true, am, ctx->hist.as<int64_t>(), nbins,
+                                  ctx->flags.as<uint32_t>(), ctx->sms, st));
+    CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, out_keys, out_sums,
+                        ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(), ctx->finscr.p, st));
+    ctx->launches += 2;
+    uint64_t m = 0;
+    CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+    CKR(launch_add_key(out_keys, m, mm, ctx->sms, st));
+    ctx->launches += 1;
+    *n_acc += m;
+    return ECC_OK;
+  }
+  CKR(launch_generic_changes(s, ECC_F32, ctx->ch8.as<int8_t>(), ctx->sms, st));
+  CKR(launch_order_keys(owned, n64, ctx->keys.as<uint32_t>(), mm, ctx->sms, st));
+  ctx->launches += 2;
+  const int bit0 = 0, bit1 = span ? 32 - __builtin_clz(span) : 1;
   size_t t1 = 0, t2 = 0;
   CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, ctx->keys.as<uint32_t>(),
                                       ctx->keys2.as<uint32_t>(), ctx->ch8.as<int8_t>(),
@@ -637,8 +668,6 @@ void write_values(ecc_dtype dtype, bool sorted, const AffineMap& am, const BinRe
 // change) list (value_index.hpp:159-197).  *used = false when the span is
 // too wide (the sort path runs instead).  The curve is left in the result
 // block (layout L); keys are bins + *key_lo.
-constexpr uint64_t kDenseKeySpan = 1ull << 24;
-
 int dense_sorted(ecc_ctx* ctx, const Slab& s, cudaStream_t st, ResultLayout* L, uint32_t* key_lo,
                  bool* used) {
   *used = false;

@@ -496,3 +496,18 @@ def test_f32_sorted_dense_and_sort_paths(ctx, case):
     import torch
     b = ctx.vcec(torch.from_numpy(img).cuda())
     assert np.array_equal(b.changes, c)
+
+
+def test_f32_sorted_dense_streamed_slabs(ctx):
+    """Streamed general f32 (>= 2^20 voxels per slab): every slab takes the
+    dense key histogram with its own key range, the runs merge on the device."""
+    rng = np.random.default_rng(8)
+    img = (2.0 + rng.random((96, 128, 256)) * 2.0 ** -7).astype(np.float32)
+    img[:, :, ::7] = np.round(img[:, :, ::7] * 256) / 256  # ties across slabs
+    v, c = oracle.vcec(img)
+    for chunks in (1, 2, 3):
+        plan = eb.plan_chunks(eb.Dims.of(img.shape), eb.ChunkTarget.count(chunks))
+        got = eb.process_image(img, plan)
+        assert np.array_equal(np.asarray(got.values, np.float32).view(np.uint32),
+                              np.asarray(v, np.float32).view(np.uint32)), chunks
+        assert np.array_equal(got.changes, c), chunks
