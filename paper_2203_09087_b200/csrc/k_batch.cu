@@ -7,12 +7,11 @@
 // (kernel.hpp:81-94) per pixel.  The per-image histogram lives in shared
 // memory:
 //   * <= 8192 bins (u8): int32 change sums + occupancy bits;
-//   * 65536 bins (u16): signed 16-bit halves packed two per word (128 KB)
-//     with exact spill: the thread whose atomic carries a half out of
-//     [-16384, 16383] subtracts what it saw and adds it to a per-SM global
-//     scratch row (one CTA per SM, so rows are private), marking the bin in
-//     a "spilled" bitmap so the epilogue reads back and re-zeroes exactly
-//     those scratch entries.
+//   * 65536 bins (u16 images wider than the bit-sliced k_batch16.cu takes):
+//     the packed biased 16-bit halves of hist16.cuh (128 KB) with exact
+//     compare-and-swap spills to a per-SM global scratch row (one CTA per
+//     SM, so rows are private), marking the bin in a "spilled" bitmap so the
+//     epilogue reads back and re-zeroes exactly those scratch entries.
 // The epilogue prefix-sums the bins in place (block scan over per-thread
 // runs) and writes the dense chi row and the occupancy bitmap -- one pass,
 // no zero-fill of the output.

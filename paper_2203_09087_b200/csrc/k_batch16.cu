@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t vmr = (X - 1 < h) ? vm : 0u;
         uint32_t V[8] = {d0 & vmr, d1 & vmr, d2 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr, d3 & vmr};
         bits::transpose8(V);
-        // histogram: groups of 4 pixels (atomic latencies overlap), one vote
+        // histogram: groups of HGRP pixels (atomic latencies overlap), one vote
         // per group for the rare out-of-band fix
         auto spill = [&](uint32_t key, int after) {
           atomicAdd(&scratch[key], after);

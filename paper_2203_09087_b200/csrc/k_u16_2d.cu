@@ -26,7 +26,10 @@
 namespace eccb {
 namespace u162d {
 
-constexpr int NW = 16;  // warps per CTA (one CTA per SM: the table fills shared memory)
+#ifndef ECC_U162D_NW
+#define ECC_U162D_NW 16
+#endif
+constexpr int NW = ECC_U162D_NW;  // warps per CTA (one CTA per SM: the table fills shared memory)
 constexpr int NT = NW * 32;
 constexpr int HWORDS = 32768, PWORDS = 2048;
 constexpr int SMEM_BYTES = (HWORDS + PWORDS) * 4;

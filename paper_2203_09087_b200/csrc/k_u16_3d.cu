@@ -18,12 +18,10 @@
 //    change in 4-bit two's complement; replicating the sign plane makes the
 //    code transpose produce signed bytes that one PRMT sign-extends.
 //  * Histogram: 65536 signed 16-bit halves packed two per word in shared
-//    memory, each biased by 32768.  A half is "in band" while its biased
-//    value lies in [16384, 49151] (bit 15 XOR bit 14 set); the thread whose
-//    atomic (which returns the old word) moves a half out of the band
-//    subtracts what it saw and adds it to the global int64 histogram.  At
-//    most 384 updates of +-7 can land between the crossing and the fix, so a
-//    half never reaches the carry boundary.  Occupancy is a 65536-bit map.
+//    memory, each biased by 32768 (hist16.cuh): an update that leaves its
+//    half outside [-8192, 8191] moves the half's current value to the global
+//    int64 histogram with a compare-and-swap, so the half is reset to exactly
+//    0 and never nears the 16-bit wrap.  Occupancy is a 65536-bit map.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
