@@ -59,7 +59,10 @@ namespace eccb {
 namespace u83d {
 using u8fin::flush_and_finalize;
 
-constexpr int NW = 4;      // warps per CTA
+#ifndef ECC_U83D_NW
+#define ECC_U83D_NW 4
+#endif
+constexpr int NW = ECC_U83D_NW;  // warps per CTA
 constexpr int NS = 4;      // TMA ring stages per warp
 constexpr int BOXZ = 48;   // box bytes along axis 2 (window of 32 + alignment)
 constexpr int BOXY = 32;   // rows per box (one per lane)
@@ -69,7 +72,10 @@ constexpr int HIST_WORDS = NCODE * 256;
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + HIST_WORDS * 4;
-constexpr int CTAS_PER_SM = 4;
+#ifndef ECC_U83D_CTAS
+#define ECC_U83D_CTAS 4
+#endif
+constexpr int CTAS_PER_SM = ECC_U83D_CTAS;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
 struct Geom {
