@@ -377,9 +377,16 @@ def main():
     alg_bytes = SIDE ** 3  # 1 B/voxel read once; the 4 KB histogram is negligible
     achieved = alg_bytes / (t_kern * 1e-3) / 1e9
     traffic = None
+    pipes = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get("k1k2_dram_bytes_per_launch")
+            nt = json.load(f)
+        traffic = nt.get("k1k2_dram_bytes_per_launch")
+        if "alu_pipe_busy_pct" in nt:
+            # what bounds the kernel instead of HBM (ncu --set full of the same kernel)
+            pipes = {"bound": "integer ALU pipe", "alu_busy_pct": nt["alu_pipe_busy_pct"],
+                     "fma_busy_pct": nt.get("fma_pipe_busy_pct"),
+                     "issue_active_pct": nt.get("issue_active_pct"), "source": nt.get("source")}
     except Exception:
         pass
 
@@ -394,6 +401,7 @@ def main():
            "kernel_ms": t_kern,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind},
+           "compute_limit": pipes,
            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e},
            "gpu_launches": launches,
