@@ -102,6 +102,67 @@ __global__ void __launch_bounds__(ROW_T)
   }
 }
 
+// The contiguous axis, pipelined: a CTA runs UPB consecutive (line, tile)
+// units and issues the next unit's loads before computing the current one,
+// so the load latency hides behind the taps (widths up to 64).
+constexpr int UPB = 8;
+
+template <int J>
+__global__ void __launch_bounds__(ROW_T)
+    k_smooth_rows_p(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
+                    uint32_t tiles, uint64_t units, const double* __restrict__ w, int width) {
+  constexpr int ROW_OUT = ROW_T * J, NV = (ROW_OUT + 63 + ROW_T - 1) / ROW_T;
+  extern __shared__ double sh[];
+  double* ws = sh;          // [width]
+  double* xs = sh + width;  // [ROW_OUT + width - 1]
+  const int half = width / 2;
+  const int ne = ROW_OUT + width - 1;
+  for (int k = threadIdx.x; k < width; k += ROW_T) ws[k] = w[k];
+  const uint64_t u0 = (uint64_t)blockIdx.x * UPB;
+  const uint64_t u1 = u0 + UPB < units ? u0 + UPB : units;
+  float v[NV];
+  auto load = [&](uint64_t u) {
+    const uint64_t line = u / tiles;
+    const int64_t p0 = (int64_t)(u - line * tiles) * ROW_OUT;
+    const float* src = in + line * L;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int e = i * ROW_T + threadIdx.x;
+      int64_t q = p0 - half + e;
+      q = q < 0 ? 0 : (q > (int64_t)L - 1 ? (int64_t)L - 1 : q);
+      v[i] = e < ne ? __ldg(src + q) : 0.0f;
+    }
+  };
+  if (u0 < u1) load(u0);
+  for (uint64_t u = u0; u < u1; ++u) {
+    __syncthreads();  // the previous unit's taps are done with xs
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int e = i * ROW_T + threadIdx.x;
+      if (e < ne) xs[e] = (double)v[i];
+    }
+    __syncthreads();
+    if (u + 1 < u1) load(u + 1);  // in flight during the taps below
+    double acc[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) acc[j] = 0.0;
+    for (int k = 0; k < width; ++k) {
+      const double wk = ws[k];
+#pragma unroll
+      for (int j = 0; j < J; ++j)
+        acc[j] = __dadd_rn(acc[j], __dmul_rn(wk, xs[threadIdx.x + ROW_T * j + k]));
+    }
+    const uint64_t line = u / tiles;
+    const int64_t p0 = (int64_t)(u - line * tiles) * ROW_OUT;
+    float* dst = out + line * L;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int64_t p = p0 + threadIdx.x + ROW_T * j;
+      if (p < (int64_t)L) dst[p] = __double2float_rn(acc[j]);
+    }
+  }
+}
+
 // inner > 1: a CTA smooths COL_W inner positions x COL_OUT outputs along the
 // axis; thread (c, g) owns column c, outputs g + COL_G j.
 constexpr int COL_W = 32, COL_G = 8, COL_J = 8, COL_OUT = COL_G * COL_J;
@@ -181,6 +242,64 @@ __global__ void __launch_bounds__(COL_W * COL_G)
   }
 }
 
+// Strided axes with a compile-time width, pipelined: a CTA runs PT
+// consecutive position tiles of one column tile and issues the next tile's
+// loads before the current tile's register-blocked taps.
+constexpr int PT = 4;
+
+template <int W>
+__global__ void __launch_bounds__(COL_W * COL_G)
+    k_smooth_cols_p(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
+                    uint64_t inner, uint32_t ctiles, uint32_t ptiles,
+                    const double* __restrict__ w) {
+  constexpr int NR = COL_OUT + W - 1, NL = (NR + COL_G - 1) / COL_G;
+  __shared__ double ws[W];
+  __shared__ double xs[NR * COL_W];
+  const int half = W / 2;
+  const uint64_t outer = blockIdx.x / ctiles;
+  const uint64_t c0 = (uint64_t)(blockIdx.x - outer * ctiles) * COL_W;
+  const float* src = in + outer * L * inner;
+  const int c = threadIdx.x & (COL_W - 1), g = threadIdx.x / COL_W;
+  const bool col_in = c0 + c < inner;
+  for (int k = threadIdx.x; k < W; k += COL_W * COL_G) ws[k] = w[k];
+  const uint32_t t0 = blockIdx.y * PT, t1 = min(t0 + PT, ptiles);
+  float v[NL];
+  auto load = [&](uint32_t t) {
+    const int64_t p0 = (int64_t)t * COL_OUT;
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int r = g + u * COL_G;
+      int64_t q = p0 - half + r;
+      q = q < 0 ? 0 : (q > (int64_t)L - 1 ? (int64_t)L - 1 : q);
+      v[u] = (col_in && r < NR) ? __ldg(src + (uint64_t)q * inner + c0 + c) : 0.0f;
+    }
+  };
+  if (t0 < t1) load(t0);
+  for (uint32_t t = t0; t < t1; ++t) {
+    __syncthreads();  // the previous tile's taps are done with xs
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int r = g + u * COL_G;
+      if (r < NR) xs[r * COL_W + c] = (double)v[u];
+    }
+    __syncthreads();
+    if (t + 1 < t1) load(t + 1);  // in flight during the taps
+    double acc[COL_J];
+#pragma unroll
+    for (int j = 0; j < COL_J; ++j) acc[j] = 0.0;
+    taps_blocked<W, COL_W>(xs, ws, g * COL_J, c, acc);
+    if (col_in) {
+      float* dst = out + outer * L * inner + c0 + c;
+      const int64_t p0 = (int64_t)t * COL_OUT;
+#pragma unroll
+      for (int j = 0; j < COL_J; ++j) {
+        const int64_t p = p0 + g * COL_J + j;
+        if (p < (int64_t)L) dst[(uint64_t)p * inner] = __double2float_rn(acc[j]);
+      }
+    }
+  }
+}
+
 }  // namespace pipe
 
 cudaError_t launch_uniform_noise(float* d, uint64_t n, uint64_t seed, int sms, cudaStream_t st) {
@@ -212,6 +331,12 @@ cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint6
       const uint64_t ctiles = (inner + COL_W - 1) / COL_W;
       const uint64_t ptiles = (L + COL_OUT - 1) / COL_OUT;
       if (outer * ctiles > 0x7FFFFFFFull || ptiles > 65535) return false;
+      if (((COL_OUT + W - 1) * COL_W + W) * 8 <= 48 * 1024) {  // static shared memory
+        k_smooth_cols_p<W><<<dim3((unsigned)(outer * ctiles), (unsigned)((ptiles + PT - 1) / PT)),
+                             COL_W * COL_G, 0, st>>>(in, out, (uint32_t)L, inner, (uint32_t)ctiles,
+                                                     (uint32_t)ptiles, d_weights);
+        return true;
+      }
       const size_t smem = (size_t)(width + (COL_OUT + width - 1) * COL_W) * 8;
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_smooth_cols<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -230,6 +355,23 @@ cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint6
     const uint64_t tiles = (L + (uint64_t)ROW_T * J - 1) / ((uint64_t)ROW_T * J);
     if (outer * tiles > 0x7FFFFFFFull) return cudaErrorInvalidValue;
     const size_t smem = (size_t)(width + ROW_T * J + width - 1) * 8;
+    const uint64_t units = outer * tiles;
+    if (width <= 64 && (units + UPB - 1) / UPB <= 0x7FFFFFFFull) {
+      const unsigned grid = (unsigned)((units + UPB - 1) / UPB);
+      auto go = [&](auto kern) {
+        if (smem > 48 * 1024)
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, ROW_T, smem, st>>>(in, out, (uint32_t)L, (uint32_t)tiles, units, d_weights,
+                                        width);
+      };
+      if (J == 1)
+        go(k_smooth_rows_p<1>);
+      else if (J == 2)
+        go(k_smooth_rows_p<2>);
+      else
+        go(k_smooth_rows_p<4>);
+      return cudaGetLastError();
+    }
     const unsigned grid = (unsigned)(outer * tiles);
     auto go = [&](auto kern) {
       if (smem > 48 * 1024)
