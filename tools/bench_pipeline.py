@@ -17,7 +17,7 @@ side = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 ref_side = int(sys.argv[3]) if len(sys.argv) > 3 else 128
 ctx = eb.context(0)
-ctx.bench_run(eb.Dims(64, 64, 64), 1)  # warm-up (allocations, module load)
+ctx.bench_run(eb.Dims(side, side, side), 1)  # warm-up at the same size (allocations, module load)
 rep = ctx.bench_run(eb.Dims(side, side, side), iters)
 out = {"impl": "b200", "dims": [side] * 3, **rep.__dict__}
 print(json.dumps(out), flush=True)
