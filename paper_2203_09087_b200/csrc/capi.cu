@@ -1081,6 +1081,77 @@ int overlapped_u8(ecc_ctx* ctx, const void* host, ecc_dims dims, cudaStream_t st
   return ECC_OK;
 }
 
+// The same overlap for the other dense maps (u16, affine f32): tapered
+// chunks copied on the copy stream, each chunk's K1+K2 on a slab view of the
+// resident volume (its planes + halo, so the f32 -> bin key pass covers just
+// those planes) as soon as it has landed, K3 after the last.
+int overlapped_dense(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims dims,
+                     const ecc_binmap* bm, cudaStream_t st, BinResult* r, AffineMap* am_out,
+                     bool* handled) {
+  *handled = false;
+  uint64_t nbins = 0;
+  bool affine = false, sorted = false;
+  AffineMap am{};
+  CKI(resolve_bins(dtype, bm, &nbins, &affine, &sorted, &am));
+  const uint64_t plane = dims.w1 * dims.w2, eb = esize(dtype), bytes = dims.w0 * plane * eb;
+  if (sorted || dtype == ECC_U8 || dims.w2 <= 1 || bytes < (32ull << 20) || dims.w0 < 8)
+    return ECC_OK;
+  int nc = (int)std::min<uint64_t>(8, std::min<uint64_t>(dims.w0 / 4, bytes >> 24));
+  nc = std::max(nc, 1);
+  std::vector<uint64_t> b(nc + 1);
+  {
+    const uint64_t tot = (uint64_t)nc * (nc + 1) / 2;
+    uint64_t acc = 0;
+    for (int k = 0; k <= nc; ++k) {
+      b[k] = dims.w0 * acc / tot;
+      if (k < nc) acc += (uint64_t)(nc - k);
+    }
+    b[nc] = dims.w0;
+    for (int k = 1; k <= nc; ++k)
+      if (b[k] <= b[k - 1]) return ECC_OK;
+  }
+  CKI(ctx->input.ensure(bytes));
+  for (int k = 0; k <= nc; ++k)
+    if (!ctx->ov_ev[k]) CKR(cudaEventCreateWithFlags(&ctx->ov_ev[k], cudaEventDisableTiming));
+  CKI(ctx->flags.ensure(16));
+  CKI(ctx->hist.ensure(2 * nbins * 8));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  CKR(cudaEventRecord(ctx->ov_ev[nc], st));
+  CKR(cudaStreamWaitEvent(ctx->copy, ctx->ov_ev[nc], 0));
+  int rc = ECC_OK;
+  for (int k = 0; k < nc && rc == ECC_OK; ++k) {
+    cudaError_t e = cudaMemcpyAsync(ctx->input.as<uint8_t>() + b[k] * plane * eb,
+                                    static_cast<const uint8_t*>(host) + b[k] * plane * eb,
+                                    (b[k + 1] - b[k]) * plane * eb, cudaMemcpyHostToDevice,
+                                    ctx->copy);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ov_ev[k], ctx->copy);
+    if (e != cudaSuccess) rc = fail(ECC_ECUDA, cudaGetErrorString(e));
+  }
+  for (int k = 0; k < nc && rc == ECC_OK; ++k) {
+    cudaError_t e = cudaStreamWaitEvent(st, ctx->ov_ev[k], 0);
+    if (e == cudaSuccess && k + 1 < nc) e = cudaStreamWaitEvent(st, ctx->ov_ev[k + 1], 0);
+    if (e != cudaSuccess) {
+      rc = fail(ECC_ECUDA, cudaGetErrorString(e));
+      break;
+    }
+    const uint64_t r0 = b[k] == 0 ? 0 : b[k] - 1;
+    const uint64_t r1 = std::min<uint64_t>(b[k + 1] + 1, dims.w0);
+    const Slab sk = make_slab(ctx->input.as<uint8_t>() + r0 * plane * eb, dims, r0, r1 - r0, b[k],
+                              b[k + 1]);
+    rc = accumulate(ctx, sk, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st);
+  }
+  if (rc == ECC_OK && affine) rc = read_flags(ctx, st);
+  if (rc == ECC_OK) rc = finalize_to_host(ctx, (uint32_t)nbins, st, r);
+  if (rc != ECC_OK) {
+    cudaStreamSynchronize(ctx->copy);
+    return rc;
+  }
+  *am_out = am;
+  *handled = true;
+  return ECC_OK;
+}
+
 static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dtype,
                          ecc_dims dims, const ecc_binmap* bm, void* values_out,
                          int64_t* series_out, uint64_t cap, uint64_t* n_out, bool want_chi) {
@@ -1096,6 +1167,8 @@ static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dt
   bool done = false;
   if (where == 0 && dtype == ECC_U8 && (!bm || bm->kind == ECC_BIN_IDENTITY))
     CKI(overlapped_u8(ctx, data, dims, st, &r, &done));
+  else if (where == 0)
+    CKI(overlapped_dense(ctx, data, dtype, dims, bm, st, &r, &am, &done));
   if (!done) {
     const void* d_data = nullptr;
     CKI(stage_input(ctx, data, where, bytes, st, &d_data));

@@ -511,3 +511,29 @@ def test_f32_sorted_dense_streamed_slabs(ctx):
         assert np.array_equal(np.asarray(got.values, np.float32).view(np.uint32),
                               np.asarray(v, np.float32).view(np.uint32)), chunks
         assert np.array_equal(got.changes, c), chunks
+
+
+@pytest.mark.parametrize("case", ["u16", "u16_odd", "f32_affine"])
+def test_overlapped_host_input_dense_maps(ctx, case):
+    """Large host volumes with the other dense maps take the overlapped path
+    (chunked H2D, per-chunk K1+K2 on slab views, K3 after the last)."""
+    rng = np.random.default_rng(len(case))
+    if case == "u16":
+        img, bm = rng.integers(0, 65536, (128, 512, 256)).astype(np.uint16), None
+    elif case == "u16_odd":
+        img, bm = rng.integers(0, 300, (100, 400, 420)).astype(np.uint16), None
+    else:
+        img = (rng.integers(0, 65536, (64, 512, 256)) * 2.0 ** -16).astype(np.float32)
+        bm = eb.quantised_binmap(65536)
+    a = ctx.vcec(img, binmap=bm) if bm else ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert np.array_equal(a.changes, c)
+    if img.dtype == np.float32:
+        assert np.array_equal(np.asarray(a.values, np.float32).view(np.uint32), v.astype(np.float32).view(np.uint32))
+    else:
+        assert np.array_equal(a.values.astype(np.int64), v.astype(np.int64))
+    if case == "f32_affine":
+        bad = img.copy()
+        bad[40, 7, 9] = 0.3
+        with pytest.raises(eb.EccError):
+            ctx.vcec(bad, binmap=bm)
