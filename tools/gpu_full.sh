@@ -12,6 +12,8 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/${TAG}_
 timeout 600 python tools/bench_configs.py C1 C3 C4 > $OUT/${TAG}_configs.jsonl 2>> $OUT/${TAG}_bench.err
 timeout 300 python tools/probe_2d.py > $OUT/${TAG}_probe_2d.txt 2>&1
 timeout 300 python tools/probe_f32.py > $OUT/${TAG}_probe_f32.txt 2>&1
+timeout 300 python tools/probe_smooth.py > $OUT/${TAG}_probe_smooth.txt 2>&1
+timeout 600 python tools/probe_e2e_dense.py > $OUT/${TAG}_probe_e2e_dense.txt 2>&1
 timeout 300 python tools/bench_pipeline.py 512 5 128 > $OUT/${TAG}_pipeline.jsonl 2>&1
 timeout 300 ./tests/cpp/bin/e2e_c > $OUT/${TAG}_e2e_c_abi.jsonl 2>&1
 timeout 600 python tools/c5_sharded.py --side 2048 > $OUT/${TAG}_c5_2048.jsonl 2>&1
