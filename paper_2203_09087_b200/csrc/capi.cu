@@ -160,6 +160,9 @@ struct ecc_xchg {
   size_t flags_off = 0, err_off = 0, bytes = 0;
   std::vector<void*> base;  // [world] opened peer buffers (own: buf)
   void* ptrs = nullptr;     // device: int64_t* slots[world] | uint32_t* flags[world]
+  uint32_t* err_host = nullptr;  // mapped pinned word the kernel raises on a peer timeout
+  uint32_t* err_dev = nullptr;   // its device alias
+  cudaStream_t last = nullptr;   // stream of the last fused launch (status syncs it)
 };
 
 namespace {
@@ -489,10 +492,38 @@ struct ToI64 {
 // order-key spans up to this many values take the dense histogram (no sort)
 constexpr uint64_t kDenseKeySpan = 1ull << 24;
 
+int merge_runs(ecc_ctx* ctx, cudaStream_t st, uint64_t n, uint64_t* m_out);
+
+// Grows a run buffer to hold `elems` elements of `esz` bytes, keeping its
+// first `keep` elements (DevBuf::ensure discards the contents).
+int grow_keep(DevBuf* b, uint64_t elems, size_t esz, uint64_t keep, cudaStream_t st) {
+  if (elems * esz <= b->cap) return ECC_OK;
+  DevBuf nb;
+  CKI(nb.ensure(elems * esz));
+  if (keep) CKR(cudaMemcpyAsync(nb.p, b->p, keep * esz, cudaMemcpyDeviceToDevice, st));
+  CKR(cudaStreamSynchronize(st));
+  b->release();
+  *b = nb;
+  return ECC_OK;
+}
+
+// Room for `add` more runs after the `*n_acc` accumulated ones.  When the
+// accumulator is full its runs are merged first (merge_local, vcec.hpp:35-66:
+// one entry per distinct value), so device memory follows the number of
+// distinct values seen so far plus one chunk -- not the image size.
+int reserve_runs(ecc_ctx* ctx, cudaStream_t st, uint64_t add, uint64_t* n_acc) {
+  const uint64_t cap = std::min(ctx->akeys.cap / 4, ctx->asums.cap / 8);
+  if (*n_acc + add <= cap) return ECC_OK;
+  if (*n_acc > 0) CKI(merge_runs(ctx, st, *n_acc, n_acc));
+  const uint64_t want = std::max(*n_acc + add, 2 * *n_acc);
+  CKI(grow_keep(&ctx->akeys, want, 4, *n_acc, st));
+  CKI(grow_keep(&ctx->asums, want, 8, *n_acc, st));
+  return ECC_OK;
+}
+
 // Appends the slab's reduced (order key, change sum) runs to the device
 // accumulator ctx->akeys / ctx->asums at offset *n (no host round trip).
-int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_voxels,
-                uint64_t* n_acc) {
+int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t* n_acc) {
   const uint64_t n64 = (uint64_t)(s.own1 - s.own0) * s.w1 * s.w2;
   if (n64 > 0x7FFFFFFFull)
     return fail(ECC_EINVAL, "chunk exceeds 2^31 voxels; use a finer chunk plan");
@@ -502,8 +533,7 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
   CKI(ctx->ch8.ensure(n64));
   CKI(ctx->ch8b.ensure(n64));
   CKI(ctx->count.ensure(8));
-  CKI(ctx->akeys.ensure(total_voxels * 4));
-  CKI(ctx->asums.ensure(total_voxels * 8));
+  CKI(reserve_runs(ctx, st, n64, n_acc));
   const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
   // flags words 1, 2: min / max order key -> dense histogram or the bit range
   // the sort must cover
@@ -578,41 +608,46 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t total_vox
 // merge_local (vcec.hpp:35-66) of every slab's runs on the device: one more
 // sort + reduce-by-key when there were several slabs, then the int64 prefix
 // sum (vcec_to_ecc) and one copy back.
-// out == nullptr: the curve stays on the device (keys in ctx->keys or
-// ctx->akeys, sums, chi in ctx->chi); *m_out gets the point count.
-int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResult* out,
-                  uint64_t* m_out = nullptr) {
+// out == nullptr: the curve stays on the device (keys in ctx->akeys, sums
+// in ctx->asums, chi in ctx->chi); *m_out gets the point count.
+// merge_local of the accumulated runs in place: sort (akeys, asums) by key
+// into (keys2, sums2), reduce-by-key back into (akeys, asums); *m_out = the
+// number of distinct keys.
+int merge_runs(ecc_ctx* ctx, cudaStream_t st, uint64_t n, uint64_t* m_out) {
+  if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "too many distinct values to merge");
   uint32_t* keys = ctx->akeys.as<uint32_t>();
   int64_t* sums = ctx->asums.as<int64_t>();
+  CKI(ctx->keys2.ensure(n * 4));
+  CKI(ctx->sums2.ensure(n * 8));
+  CKI(ctx->count.ensure(8));
+  size_t t1 = 0, t2 = 0;
+  CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, ctx->keys2.as<uint32_t>(), sums,
+                                      ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
+  CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(), keys,
+                                     ctx->sums2.as<int64_t>(), sums, ctx->count.as<uint64_t>(),
+                                     cub::Sum(), (int)n, st));
+  CKI(ctx->tmp.ensure(std::max(t1, t2)));
+  t1 = ctx->tmp.cap;
+  CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, keys, ctx->keys2.as<uint32_t>(), sums,
+                                      ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
+  t2 = ctx->tmp.cap;
+  CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(), keys,
+                                     ctx->sums2.as<int64_t>(), sums, ctx->count.as<uint64_t>(),
+                                     cub::Sum(), (int)n, st));
+  ctx->launches += 2;
+  uint64_t m = 0;
+  CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  *m_out = m;
+  return ECC_OK;
+}
+
+int sorted_finish(ecc_ctx* ctx, cudaStream_t st, uint64_t n, bool merge, BinResult* out,
+                  uint64_t* m_out = nullptr) {
   uint64_t m = n;
-  if (merge && n > 0) {
-    if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "too many distinct values to merge");
-    CKI(ctx->keys.ensure(n * 4));
-    CKI(ctx->keys2.ensure(n * 4));
-    CKI(ctx->sums.ensure(n * 8));
-    CKI(ctx->sums2.ensure(n * 8));
-    size_t t1 = 0, t2 = 0;
-    CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, ctx->keys2.as<uint32_t>(), sums,
-                                        ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
-    CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys2.as<uint32_t>(),
-                                       ctx->keys.as<uint32_t>(), ctx->sums2.as<int64_t>(),
-                                       ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(),
-                                       cub::Sum(), (int)n, st));
-    CKI(ctx->tmp.ensure(std::max(t1, t2)));
-    t1 = ctx->tmp.cap;
-    CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, keys, ctx->keys2.as<uint32_t>(), sums,
-                                        ctx->sums2.as<int64_t>(), (int)n, 0, 32, st));
-    t2 = ctx->tmp.cap;
-    CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys2.as<uint32_t>(),
-                                       ctx->keys.as<uint32_t>(), ctx->sums2.as<int64_t>(),
-                                       ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(),
-                                       cub::Sum(), (int)n, st));
-    ctx->launches += 2;
-    CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
-    CKR(cudaStreamSynchronize(st));
-    keys = ctx->keys.as<uint32_t>();
-    sums = ctx->sums.as<int64_t>();
-  }
+  if (merge && n > 0) CKI(merge_runs(ctx, st, n, &m));
+  const uint32_t* keys = ctx->akeys.as<uint32_t>();
+  const int64_t* sums = ctx->asums.as<int64_t>();
   CKI(ctx->chi.ensure(std::max<uint64_t>(m, 1) * 8));
   if (m > 0) {
     size_t t3 = 0;
@@ -746,7 +781,7 @@ int run_volume(ecc_ctx* ctx, const void* d_data, ecc_dtype dtype, ecc_dims dims,
       return ECC_OK;
     }
     uint64_t n = 0;
-    CKI(sorted_slab(ctx, s, st, dims.w0 * dims.w1 * dims.w2, &n));
+    CKI(sorted_slab(ctx, s, st, &n));
     CKI(read_flags(ctx, st));
     return sorted_finish(ctx, st, n, false, res);
   }
@@ -1161,6 +1196,10 @@ static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dt
   if (!data || !values_out || !series_out || !n_out) return fail(ECC_EINVAL, "null pointer");
   cudaStream_t st = ctx->stream;
   const uint64_t bytes = dims.w0 * dims.w1 * dims.w2 * esize(dtype);
+  // every path reports the error flags of THIS call (fetch_result copies
+  // them into the result block): clear what an earlier rejected call left
+  CKI(ctx->flags.ensure(16));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
   BinResult r;
   bool sorted = false;
   AffineMap am{};
@@ -1315,7 +1354,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
     const Slab s = make_slab(ctx->slab[b].p, dims, r0, r1 - r0, own0, own1);
     t.merge_begin = since();
     if (sorted) {
-      CKI(sorted_slab(ctx, s, st, dims.w0 * dims.w1 * dims.w2, &sorted_n));
+      CKI(sorted_slab(ctx, s, st, &sorted_n));
     } else {
       CKI(accumulate(ctx, s, dtype, affine, am, (uint32_t)nbins, ctx->hist.as<int64_t>(), st));
     }
@@ -1709,7 +1748,7 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
       last_chi = ctx->res.as<uint8_t>() + L.chi;
     } else if (rc == ECC_OK) {
       uint64_t nacc = 0;
-      rc = sorted_slab(ctx, s, st, n, &nacc);
+      rc = sorted_slab(ctx, s, st, &nacc);
       if (rc == ECC_OK) rc = read_flags(ctx, st);
       if (rc == ECC_OK) rc = sorted_finish(ctx, st, nacc, false, nullptr, &m);
       last_chi = ctx->chi.as<uint8_t>();
@@ -1811,6 +1850,18 @@ int ecc_xchg_create(ecc_ctx* ctx, int rank, int world, ecc_xchg** out, void* han
     return fail(ECC_ECUDA, std::string("exchange buffer: ") + cudaGetErrorString(e));
   }
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  if (e == cudaSuccess)
+    e = cudaHostAlloc(reinterpret_cast<void**>(&x->err_host), 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *x->err_host = 0;
+    e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&x->err_dev), x->err_host, 0);
+  }
+  if (e != cudaSuccess) {
+    if (x->err_host) cudaFreeHost(x->err_host);
+    cudaFree(x->buf);
+    delete x;
+    return fail(ECC_ECUDA, std::string("exchange error word: ") + cudaGetErrorString(e));
+  }
   std::memcpy(handle_out, &h, 64);
   *out = x;
   return ECC_OK;
@@ -1850,16 +1901,16 @@ void ecc_xchg_destroy(ecc_xchg* x) {
     if (r != x->rank && x->base[r]) cudaIpcCloseMemHandle(x->base[r]);
   if (x->ptrs) cudaFree(x->ptrs);
   if (x->buf) cudaFree(x->buf);
+  if (x->err_host) cudaFreeHost(x->err_host);
   delete x;
 }
 
 int ecc_xchg_status(ecc_xchg* x) {
   if (!x) return fail(ECC_EINVAL, "null exchange");
   CKI(bind(x->ctx));
-  uint32_t err = 0;
-  CKR(cudaStreamSynchronize(x->ctx->stream));
-  CKR(cudaMemcpy(&err, static_cast<uint8_t*>(x->buf) + x->err_off, 4, cudaMemcpyDeviceToHost));
-  if (err) return fail(ECC_ECUDA, "rank exchange timed out: a peer never published its histogram");
+  CKR(cudaStreamSynchronize(x->last ? x->last : x->ctx->stream));
+  if (*reinterpret_cast<volatile uint32_t*>(x->err_host))
+    return fail(ECC_ECUDA, "rank exchange timed out: a peer never published its histogram");
   return ECC_OK;
 }
 
@@ -1871,6 +1922,10 @@ int ecc_curve_sharded(ecc_ctx* ctx, ecc_xchg* x, const void* d_planes, ecc_dims 
   CKI(check_dims(image));
   CKI(check_slab(image, plane0, nplanes, own0, own1));
   if (!x || !x->ptrs) return fail(ECC_EINVAL, "exchange not opened");
+  // a peer timed out in an earlier launch: this rank's step count is out of
+  // step with its peers, so no later curve could be trusted
+  if (*reinterpret_cast<volatile uint32_t*>(x->err_host))
+    return fail(ECC_ECUDA, "rank exchange timed out: a peer never published its histogram");
   if (!d_planes || !d_bins || !d_changes || !d_chi || !d_count)
     return fail(ECC_EINVAL, "null device pointer");
   const Slab s = make_slab(d_planes, image, plane0, nplanes, own0, own1);
@@ -1889,7 +1944,8 @@ int ecc_curve_sharded(ecc_ctx* ctx, ecc_xchg* x, const void* d_planes, ecc_dims 
   fz.flags = reinterpret_cast<uint32_t* const*>(static_cast<void**>(x->ptrs) + x->world);
   fz.my_slots = static_cast<const int64_t*>(x->buf);
   fz.my_flags = reinterpret_cast<const uint32_t*>(static_cast<uint8_t*>(x->buf) + x->flags_off);
-  fz.err = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(x->buf) + x->err_off);
+  fz.err = x->err_dev;
+  x->last = st;
   CKR(launch_u8_3d(s, reinterpret_cast<int64_t*>(ctx->fused.as<uint8_t>() + 256), nullptr,
                    ctx->sms, st, &fz));
   ctx->launches += 1;

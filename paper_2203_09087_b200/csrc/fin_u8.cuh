@@ -28,7 +28,7 @@ struct Xchg {
   uint32_t* const* flags = nullptr;  // [world] -> peer's uint32[2][world]
   const int64_t* my_slots = nullptr;
   const uint32_t* my_flags = nullptr;
-  uint32_t* err = nullptr;      // set when a peer never arrives (timeout)
+  uint32_t* err = nullptr;      // mapped host word: set when a peer never arrives (timeout)
 };
 
 struct Fin {
@@ -98,19 +98,35 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
     }
     __threadfence_system();
     __syncthreads();
+    __shared__ int timed_out;
     if (threadIdx.x == 0) {
+      timed_out = 0;
       for (int r = 0; r < x.world; ++r) st_release_sys(x.flags[r] + par * x.world + x.rank, x.epoch);
       // wait for every rank's data in our own buffer (10 s guard: never hang)
       const uint64_t t0 = globaltimer();
-      for (int r = 0; r < x.world; ++r)
+      for (int r = 0; r < x.world && !timed_out; ++r)
         while (ld_acquire_sys(x.my_flags + par * x.world + r) != x.epoch) {
           if (globaltimer() - t0 > 10000000000ull) {
-            atomicExch(x.err, 1u);
+            timed_out = 1;
             break;
           }
         }
     }
     __syncthreads();
+    if (timed_out) {
+      // no partial curve: the count is poisoned (the host API rejects a
+      // count above 256), the flag is raised in mapped host memory so the
+      // NEXT ecc_curve_sharded call fails without a device round trip, and
+      // the workspace is re-zeroed like on the normal path
+      for (int v = threadIdx.x; v < 512; v += NT) ghist[v] = 0;
+      if (threadIdx.x == 0) {
+        *fin.count = ~0ull;
+        *reinterpret_cast<volatile uint32_t*>(x.err) = 1u;
+        __threadfence_system();
+        *fin.ticket = 0;
+      }
+      return;
+    }
   }
   // the global histogram: this launch's (one rank) or the sum of all ranks'
   auto gsum = [&](int v) -> long long {
