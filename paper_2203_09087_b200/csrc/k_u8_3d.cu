@@ -63,7 +63,10 @@ using u8fin::flush_and_finalize;
 #define ECC_U83D_NW 4
 #endif
 constexpr int NW = ECC_U83D_NW;  // warps per CTA
-constexpr int NS = 4;      // TMA ring stages per warp
+#ifndef ECC_U83D_NS
+#define ECC_U83D_NS 4
+#endif
+constexpr int NS = ECC_U83D_NS;  // TMA ring stages per warp (a power of two)
 constexpr int BOXZ = 48;   // box bytes along axis 2 (window of 32 + alignment)
 constexpr int BOXY = 32;   // rows per box (one per lane)
 constexpr int STAGE = BOXZ * BOXY;
@@ -220,12 +223,12 @@ struct Codes {
 // changes of P (X-1 is an owned plane).
 template <bool CH, int KIND, class Issue>
 __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int zs,
-                                           const RunGeom& rg, int& step,
+                                           const RunGeom& rg, uint32_t& step,
                                            uint8_t (*myring)[STAGE], uint64_t* myfull,
-                                           uint32_t* hist, const Cursor& pc, int lane,
+                                           const uint32_t hist_s, const Cursor& pc, int lane,
                                            Row& P, Row& N, XCarry& xc, Issue& issue) {
-  const int slot = step & (NS - 1);
-  const uint32_t phase = (uint32_t)((step / NS) & 1);
+  const uint32_t slot = step & (NS - 1);
+  const uint32_t phase = (step / NS) & 1u;
   mbar_wait(&myfull[slot], phase);
   {
     const uint4* rowp = reinterpret_cast<const uint4*>(myring[slot] + lane * BOXZ);
@@ -245,10 +248,10 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
 #undef ECC_WINDOW
   }
   __syncwarp();
-  if (pc.valid(g)) {  // refill this slot with the load NS steps ahead
-    if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    issue(slot);
-  }
+  // refill this slot with the load NS steps ahead.  Every lane has consumed
+  // its LDS results (the funnel shifts above) before the __syncwarp, so the
+  // async-proxy write cannot overtake a generic read of the slot.
+  if (pc.valid(g)) issue(slot);
   uint32_t (&C)[8] = N.C;
   bits::byte_interleave(N.W, C);
   bits::transpose8(C);
@@ -322,26 +325,36 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
       uint32_t s[4];
       bits::sum_code(w1, w2, s);
       const uint32_t vm = rg.vm;
-      const uint32_t hist_s = smem_u32(hist);
       uint32_t V[8];
       bits::transpose_codes(s[0] & vm, s[1] & vm, s[2] & vm, s[3] | ~vm, V);
+      if constexpr (CH) {
 #pragma unroll
-      for (int p = 1; p <= 30; ++p) {
-        const int r = p & 7, b = p >> 3;
-        const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
-                                        (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
-        if constexpr (CH) {
+        for (int p = 1; p <= 30; ++p) {
+          const int r = p & 7, b = p >> 3;
+          const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
+                                          (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
           if ((vm >> p) & 1) {
             const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + (zs - 1) + p;
             g.chg[vox] = (int8_t)decode_change(idx >> 8);
           }
-        } else {
-          // address = hist + 4 * idx on the FMA pipe (IMAD) rather than an
-          // ALU-pipe LEA: the integer ALU pipe is this kernel's bottleneck
+        }
+      } else {
+        // one shared-memory increment per voxel at hist[code][value]; the
+        // address (hist + 4 * idx) is an IMAD on the FMA pipe rather than an
+        // ALU-pipe LEA (the integer ALU pipe is this kernel's bottleneck).
+        // (Predicating the halo lanes' atomics off through grouped asm was
+        // measured slower: 161 vs 141 us, the grouping serialises the
+        // address computation.)
+#pragma unroll
+        for (int p = 1; p <= 30; ++p) {
+          const int r = p & 7, b = p >> 3;
+          const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
+                                          (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
           uint32_t addr;
           asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(idx), "r"(g.four), "r"(hist_s));
           asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
         }
+
       }
     }
     xc.gxa = gxa; xc.gxz = gxz; xc.gxz1 = gxz1; xc.gxy = gxy; xc.gxyu = gxyu;
@@ -389,22 +402,23 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
   Row A, B;
   XCarry xc;
   RunGeom rg;
-  int step = 0;
+  uint32_t step = 0;
+  const uint32_t hist_s = smem_u32(hist);
   for (int u = gw; u < g.nunits; u += nwt) {
     Cursor cc;
     cc.start(g, u);
     rg.set(g, cc, lane);
     const int x0 = cc.x0, zs = cc.zs, len = cc.len;
-    sweep_step<CH, 0>(g, x0 - 1, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
-    sweep_step<CH, 1>(g, x0, zs, rg, step, myring, myfull, hist, pc, lane, A, B, xc, issue);
+    sweep_step<CH, 0>(g, x0 - 1, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
+    sweep_step<CH, 1>(g, x0, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
     // planes x0+1 .. x0+len: the changes of x0 .. x0+len-1
     int X = x0 + 1;
     for (; X + 1 <= x0 + len; X += 2) {
-      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
-      sweep_step<CH, 2>(g, X + 1, zs, rg, step, myring, myfull, hist, pc, lane, A, B, xc, issue);
+      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
+      sweep_step<CH, 2>(g, X + 1, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
     }
     if (X <= x0 + len)
-      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist, pc, lane, B, A, xc, issue);
+      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
   }
   if constexpr (!CH) flush_and_finalize<NW * 32, Codes>(hist, ghist, fin);
 }
