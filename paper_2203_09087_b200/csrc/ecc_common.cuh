@@ -48,57 +48,6 @@ enum : uint32_t {
   kFlagNaN = 2u,
 };
 
-// ---------------------------------------------------------------------------
-// Per-voxel change, 3D (kernel.hpp:99-137).  w[a][b][c] is the neighbour at
-// offset (a-1, b-1, c-1) along (axis0, axis1, axis2).  Offsets whose first
-// nonzero component is negative are earlier in row-major order
-// (kernel.hpp:21-27) and compare strictly.
-__device__ __forceinline__ int change3(const uint32_t (&w)[3][3][3]) {
-  const uint32_t c = w[1][1][1];
-  const unsigned xm = c < w[0][1][1], xp = c <= w[2][1][1];
-  const unsigned ym = c < w[1][0][1], yp = c <= w[1][2][1];
-  const unsigned zm = c < w[1][1][0], zp = c <= w[1][1][2];
-  const unsigned exy_mm = xm & ym & (unsigned)(c < w[0][0][1]);
-  const unsigned exy_mp = xm & yp & (unsigned)(c < w[0][2][1]);
-  const unsigned exy_pm = xp & ym & (unsigned)(c <= w[2][0][1]);
-  const unsigned exy_pp = xp & yp & (unsigned)(c <= w[2][2][1]);
-  const unsigned exz_mm = xm & zm & (unsigned)(c < w[0][1][0]);
-  const unsigned exz_mp = xm & zp & (unsigned)(c < w[0][1][2]);
-  const unsigned exz_pm = xp & zm & (unsigned)(c <= w[2][1][0]);
-  const unsigned exz_pp = xp & zp & (unsigned)(c <= w[2][1][2]);
-  const unsigned eyz_mm = ym & zm & (unsigned)(c < w[1][0][0]);
-  const unsigned eyz_mp = ym & zp & (unsigned)(c < w[1][0][2]);
-  const unsigned eyz_pm = yp & zm & (unsigned)(c <= w[1][2][0]);
-  const unsigned eyz_pp = yp & zp & (unsigned)(c <= w[1][2][2]);
-  unsigned v = 0;
-  v += exy_mm & exz_mm & eyz_mm & (unsigned)(c < w[0][0][0]);
-  v += exy_mm & exz_mp & eyz_mp & (unsigned)(c < w[0][0][2]);
-  v += exy_mp & exz_mm & eyz_pm & (unsigned)(c < w[0][2][0]);
-  v += exy_mp & exz_mp & eyz_pp & (unsigned)(c < w[0][2][2]);
-  v += exy_pm & exz_pm & eyz_mm & (unsigned)(c <= w[2][0][0]);
-  v += exy_pm & exz_pp & eyz_mp & (unsigned)(c <= w[2][0][2]);
-  v += exy_pp & exz_pm & eyz_pm & (unsigned)(c <= w[2][2][0]);
-  v += exy_pp & exz_pp & eyz_pp & (unsigned)(c <= w[2][2][2]);
-  const unsigned sq = xm + xp + ym + yp + zm + zp;
-  const unsigned ed = exy_mm + exy_mp + exy_pm + exy_pp + exz_mm + exz_mp +
-                      exz_pm + exz_pp + eyz_mm + eyz_mp + eyz_pm + eyz_pp;
-  return -1 + (int)sq - (int)ed + (int)v;
-}
-
-// Per-voxel change, 2D over axes 0 and 1 (kernel.hpp:81-94).  w[a][b] is the
-// neighbour at offset (a-1, b-1).
-__device__ __forceinline__ int change2(const uint32_t (&w)[3][3]) {
-  const uint32_t c = w[1][1];
-  const unsigned am = c < w[0][1], ap = c <= w[2][1];
-  const unsigned bm = c < w[1][0], bp = c <= w[1][2];
-  unsigned v = 0;
-  v += am & bm & (unsigned)(c < w[0][0]);
-  v += am & bp & (unsigned)(c < w[0][2]);
-  v += ap & bm & (unsigned)(c <= w[2][0]);
-  v += ap & bp & (unsigned)(c <= w[2][2]);
-  return 1 + (int)v - (int)(am + ap + bm + bp);
-}
-
 // Affine f32 bin map: bin = (v - lo) * inv_step must be an exact integer in
 // [0, nbins) whose inverse lo + bin * step reproduces v (== compares -0 and
 // +0 equal, so -0 lands on +0's bin as in value_index.hpp:97).  The inverse
@@ -112,6 +61,11 @@ struct AffineMap {
   // (value_index.hpp:95-99 order, every distinct value its own bin)
   int keyed = 0;
   uint32_t key_lo = 0;
+  // value-index map (ValueIndex<float>::bin_of, value_index.hpp:40-45): bin =
+  // position of the value's order key in this ascending device table, which
+  // must hold it exactly (else ECC_EBINMAP)
+  const uint32_t* table = nullptr;
+  uint32_t table_n = 0;
 };
 
 __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,

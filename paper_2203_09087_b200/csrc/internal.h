@@ -63,6 +63,9 @@ cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
                                       cudaStream_t st);
 cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sms,
                                    cudaStream_t st);
+// per owned voxel, the mask of FaceOffsets it introduces (tourney.cuh faces3)
+cudaError_t launch_generic_faces(const Slab& s, int dtype, uint32_t* out, int sms,
+                                 cudaStream_t st);
 // sorted f32 path: key range (+ NaN flag), keys minus the minimum, and the
 // minimum added back to the reduced keys
 cudaError_t launch_key_range(const float* v, uint64_t n, uint32_t* flags, uint32_t* mm, int sms,

@@ -2,9 +2,10 @@
 // in-memory batched entry point; BASELINE config 3 needs one).
 //
 // One CTA per image (1024 threads).  Thread t owns column j = t % w of a
-// band of rows and slides a 3 x 3 key window down it (one new row of three
-// values per step, prefetched one step ahead), evaluating change_2d
-// (kernel.hpp:81-94) per pixel.  The per-image histogram lives in shared
+// band of rows and slides a window of three rows of (j-1, j, j+1) keys down
+// it (one new row per step, prefetched one step ahead), carrying each row's
+// in-row block minima and deciding the pixel's blocks by the tournament of
+// tourney.cuh (the 2D stencil of kernel.hpp:81-94).  The per-image histogram lives in shared
 // memory:
 //   * <= 8192 bins (u8): int32 change sums + occupancy bits;
 //   * 65536 bins (u16 images wider than the bit-sliced k_batch16.cu takes):
@@ -20,6 +21,7 @@
 #include "ecc_common.cuh"
 #include "hist16.cuh"
 #include "internal.h"
+#include "tourney.cuh"
 
 namespace eccb {
 
@@ -31,16 +33,6 @@ __device__ __forceinline__ uint32_t smid() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
-}
-
-// change_2d over axes 0 and 1 (kernel.hpp:81-94): w[a][b] = offset (a-1, b-1)
-__device__ __forceinline__ int change2k(const uint32_t (&w)[3][3]) {
-  const uint32_t c = w[1][1];
-  const int am = c < w[0][1], ap = c <= w[2][1];
-  const int bm = c < w[1][0], bp = c <= w[1][2];
-  const int v = (am & bm & (c < w[0][0])) + (am & bp & (c < w[0][2])) +
-                (ap & bm & (c <= w[2][0])) + (ap & bp & (c <= w[2][2]));
-  return 1 + v - (am + ap + bm + bp);
 }
 
 }  // namespace
@@ -88,18 +80,20 @@ __global__ void __launch_bounds__(NT, 1)
       r[1] = (uint32_t)__ldg(q);
       r[2] = rv ? (uint32_t)__ldg(q + 1) : SENT;
     };
-    uint32_t win[3][3], nxt[3];
-    fetch(i0 - 1, p, win[0]);
-    fetch(i0, p + w, win[1]);
+    uint32_t r0[3], r1[3], nxt[3];
+    fetch(i0 - 1, p, r0);
+    fetch(i0, p + w, r1);
     fetch(i0 + 1, p + 2 * w, nxt);
     p += 3 * w;  // row i0 + 2
+    tour::Plane<tour::NB2> prev = tour::row2(r0[0], r0[1], r0[2]);
+    tour::Plane<tour::NB2> cur = tour::row2(r1[0], r1[1], r1[2]);
+    uint32_t Xp = tour::xmask(cur, prev);
     for (int i = i0; i < i1; ++i, p += w) {
-      win[2][0] = nxt[0];
-      win[2][1] = nxt[1];
-      win[2][2] = nxt[2];
+      const tour::Plane<tour::NB2> next = tour::row2(nxt[0], nxt[1], nxt[2]);
       fetch(i + 2, p, nxt);  // prefetch
-      const int ch = change2k(win);
-      const uint32_t v = win[1][1];
+      const uint32_t X = tour::xmask(next, cur);
+      const int ch = tour::change_of<tour::POS2>(cur.I, X, Xp);
+      const uint32_t v = cur.M[0];
       // occupancy: a plain load first; the atomic only the first time
       if (!((pres[v >> 5] >> (v & 31)) & 1u)) atomicOr(&pres[v >> 5], 1u << (v & 31));
       if (ch != 0) {
@@ -117,11 +111,8 @@ __global__ void __launch_bounds__(NT, 1)
           atomicAdd(&bins[v], (uint32_t)ch);
         }
       }
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        win[0][b] = win[1][b];
-        win[1][b] = win[2][b];
-      }
+      Xp = X;
+      cur = next;
     }
   }
   __syncthreads();

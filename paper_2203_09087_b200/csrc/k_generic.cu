@@ -1,39 +1,38 @@
 // k_generic.cu -- the general-shape stencil kernels (any dims, any slab, any
 // value type) and the K3 finalize kernel.
 //
-// These serve every shape the specialised kernels (k_u8_3d.cu, k_bins.cu)
-// do not: ragged dims, thin slabs, f32 general binning.  One thread owns one
-// axis-0 column (one (j,k) position in 3D, one j in 2D) and sweeps a segment
-// of owned planes with a 3x3(x3) key window in registers, so each neighbour
-// value is loaded once per plane step (the row-oriented traversal of
-// change_row_3d, kernel.hpp:143-188, turned sideways).
+// These serve every shape the bit-sliced kernels (k_u8_3d.cu, k_u16_3d.cu,
+// k_u8_2d.cu, k_u16_2d.cu) do not take: ragged dims, thin slabs, the general
+// (sorted) f32 path, value-index tables, and the per-face masks behind the
+// C++ introduced().  They evaluate the scalar tournament of tourney.cuh: one
+// thread per axis-1/axis-2 position (3D) or axis-1 position (2D) sweeps a
+// segment of axis-0 planes carrying the previous plane's block minima, so a
+// plane step costs three key loads (3D), the in-plane tournament on
+// warp-shuffled neighbours, nine minimum-vs-minimum comparisons along axis 0
+// and two popcounts.  Lanes 0 and 31 of a warp are halo (their keys feed the
+// neighbouring lanes' blocks); lanes 1..30 own voxels.
 #include <cub/cub.cuh>
 
 #include "ecc_common.cuh"
 #include "internal.h"
+#include "tourney.cuh"
 
 namespace eccb {
 
-template <class T>
-__device__ __forceinline__ uint32_t ldkey(const Slab& s, int64_t i, int64_t j,
-                                          int64_t k) {
-  if (i < 0 || i >= s.w0 || j < 0 || j >= s.w1 || k < 0 || k >= s.w2)
-    return KeyTraits<T>::kSentinel;
-  const T* p = static_cast<const T*>(s.base);
-  return KeyTraits<T>::key(__ldg(p + ((i - s.plane0) * s.w1 + j) * s.w2 + k));
-}
-
-template <class T>
-__device__ __forceinline__ T ldval(const Slab& s, int64_t i, int64_t j,
-                                   int64_t k) {
-  const T* p = static_cast<const T*>(s.base);
-  return __ldg(p + ((i - s.plane0) * s.w1 + j) * s.w2 + k);
-}
-
 template <class T, bool AFFINE>
-__device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am,
-                                           uint32_t* flags) {
+__device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am, uint32_t* flags) {
   if constexpr (AFFINE) {
+    if (am.table) {  // ValueIndex::bin_of (value_index.hpp:40-45): exact match in the table
+      const uint32_t k = float_order_key_bits(__float_as_uint(static_cast<float>(v)));
+      uint32_t lo = 0, hi = am.table_n;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (am.table[mid] < k) lo = mid + 1; else hi = mid;
+      }
+      if (lo < am.table_n && am.table[lo] == k) return lo;
+      atomicOr(flags, v != v ? kFlagNaN : kFlagBinmap);
+      return 0;
+    }
     if (am.keyed)  // dense sorted-f32 path: the order key relative to the minimum
       return float_order_key_bits(__float_as_uint(static_cast<float>(v))) - am.key_lo;
     return affine_bin(am, static_cast<float>(v), flags);
@@ -95,103 +94,164 @@ __device__ __forceinline__ void sink_flush(HistSink<SMEM>& h) {
   }
 }
 
+// What a generic launch produces.
+enum Mode : int {
+  kHistSmem = 0,   // per-bin change sums + counts, shared bins flushed per CTA
+  kHistGlobal = 1, // same, straight to the global int64 histogram
+  kChanges = 2,    // int8 change per owned voxel (compute_changes)
+  kFaces = 3       // uint32 introduced-face mask per owned voxel (tourney.cuh faces3/faces2)
+};
+
+constexpr uint32_t FULLMASK = 0xFFFFFFFFu;
+constexpr int LANES_OWNED = 30;  // lanes 1..30 of a warp own voxels
+
 // ---------------------------------------------------------------- 3D
-// block (32, BY): threadIdx.x -> axis 2, threadIdx.y -> axis 1;
-// blockIdx.z -> segment of `seg` owned planes.
-template <class T, bool AFFINE, bool SMEM, bool HIST>
-__global__ void k_generic3(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
-                           uint32_t nbins, uint32_t* flags, int8_t* changes) {
+// block (32, BY): lane -> axis 2 (k = 30 * blockIdx.x + lane - 1), threadIdx.y
+// -> axis 1 (one row j per warp); blockIdx.z -> segment of `seg` owned planes.
+template <class T, bool AFFINE, int MODE>
+__global__ void __launch_bounds__(256) k_tour3(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
+                                               uint32_t nbins, uint32_t* flags, void* out) {
   extern __shared__ int32_t sh[];
-  HistSink<SMEM> sink;
-  if constexpr (HIST) sink_init<SMEM>(sink, ghist, nbins, sh);
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal;
+  HistSink<MODE == kHistSmem> sink;
+  if constexpr (HIST) sink_init(sink, ghist, nbins, sh);
+  constexpr uint32_t SENT = KeyTraits<T>::kSentinel;
+  const int lane = threadIdx.x;
+  const int64_t k = (int64_t)blockIdx.x * LANES_OWNED + lane - 1;
   const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
   const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
   const int64_t i1 = min(i0 + seg, s.own1);
-  if (j < s.w1 && k < s.w2 && i0 < i1) {
-    // per-thread: which in-plane neighbours exist (mask bit 3b + c) and the
-    // element offset of the centre of plane i (+ i * plane); no per-load
-    // 64-bit index products or 6-way bounds tests
-    uint32_t inb = 0;
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-      for (int c = 0; c < 3; ++c)
-        if (j - 1 + b >= 0 && j - 1 + b < s.w1 && k - 1 + c >= 0 && k - 1 + c < s.w2)
-          inb |= 1u << (3 * b + c);
-    const T* base = static_cast<const T*>(s.base);
-    const int64_t plane = s.w1 * s.w2, row = s.w2;
-    const T* ctr = base + (j * s.w2 + k) - s.plane0 * plane;
-    auto load_plane = [&](int64_t ii, uint32_t (&out)[3][3]) {
-      const uint32_t m = (ii >= 0 && ii < s.w0) ? inb : 0u;
-      const T* pc = ctr + ii * plane;
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-          out[b][c] = ((m >> (3 * b + c)) & 1u)
-                          ? KeyTraits<T>::key(__ldg(pc + (b - 1) * row + (c - 1)))
-                          : KeyTraits<T>::kSentinel;
-    };
-    uint32_t w[3][3][3];
-    load_plane(i0 - 1, w[0]);
-    load_plane(i0, w[1]);
-    for (int64_t i = i0; i < i1; ++i) {
-      load_plane(i + 1, w[2]);
-      const int ch = change3(w);
-      if constexpr (HIST) {
-        const T v = ldval<T>(s, i, j, k);
-        sink.add(bin_of<T, AFFINE>(v, am, flags), ch);
-      } else {
-        changes[((i - s.own0) * s.w1 + j) * s.w2 + k] = static_cast<int8_t>(ch);
+  if (j < s.w1 && i0 < i1) {  // warp-uniform (a warp is one row j)
+    const bool kin = k >= 0 && k < s.w2;
+    const bool own = kin && lane >= 1 && lane <= LANES_OWNED;
+    const bool up = j > 0, dn = j + 1 < s.w1;
+    const int64_t rp = s.row_pitch(), pp = s.plane_pitch();
+    const T* ctr = static_cast<const T*>(s.base) + j * rp + (kin ? k : 0) - s.plane0 * pp;
+
+    // block minima and in-plane wins of plane i for this lane's voxel
+    auto plane = [&](int64_t i, tour::Plane<tour::NB3>& P, T& val) {
+      uint32_t am_ = SENT, a0 = SENT, ap = SENT;
+      if (kin && i >= 0 && i < s.w0) {
+        const T* pc = ctr + i * pp;
+        val = __ldg(pc);
+        a0 = KeyTraits<T>::key(val);
+        if (up) am_ = KeyTraits<T>::key(__ldg(pc - rp));
+        if (dn) ap = KeyTraits<T>::key(__ldg(pc + rp));
       }
-#pragma unroll
-      for (int b = 0; b < 3; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          w[0][b][c] = w[1][b][c];
-          w[1][b][c] = w[2][b][c];
+      // the same rows at k + 1 (lane + 1)
+      const uint32_t bm_ = __shfl_down_sync(FULLMASK, am_, 1);
+      const uint32_t b0 = __shfl_down_sync(FULLMASK, a0, 1);
+      const uint32_t bp = __shfl_down_sync(FULLMASK, ap, 1);
+      // pairs along axis 2 anchored at k (rows j-1, j, j+1)
+      const uint32_t mzm = min(am_, bm_), mz0 = min(a0, b0), mzp = min(ap, bp);
+      const bool hz0 = b0 < a0;        // k+1 beats k in row j
+      // pairs along axis 1 anchored at (j-1, k) and (j, k)
+      const bool hym = a0 < am_, hy0 = ap < a0;
+      // 2 x 2 blocks anchored at (j-1, k), (j, k): the later row's pair wins?
+      const bool hqm = mz0 < mzm, hq0 = mzp < mz0;
+      const uint32_t mqm = min(mzm, mz0), mq0 = min(mz0, mzp);
+      // the blocks anchored at k - 1 come from lane - 1
+      const uint32_t Lmz0 = __shfl_up_sync(FULLMASK, mz0, 1);
+      const uint32_t Lmqm = __shfl_up_sync(FULLMASK, mqm, 1);
+      const uint32_t Lmq0 = __shfl_up_sync(FULLMASK, mq0, 1);
+      const uint32_t Lb = __shfl_up_sync(FULLMASK, (uint32_t)hz0 | ((uint32_t)hqm << 1) |
+                                                       ((uint32_t)hq0 << 2), 1);
+      const uint32_t Lhz0 = Lb & 1u, Lhqm = (Lb >> 1) & 1u, Lhq0 = (Lb >> 2) & 1u;
+      const uint32_t nz0 = !hz0;
+      P.M[0] = a0;   P.M[1] = Lmz0; P.M[2] = mz0; P.M[3] = min(am_, a0); P.M[4] = min(a0, ap);
+      P.M[5] = Lmqm; P.M[6] = mqm;  P.M[7] = Lmq0; P.M[8] = mq0;
+      P.I = 1u | (Lhz0 << 1) | (nz0 << 2) | ((uint32_t)hym << 3) | ((uint32_t)!hy0 << 4) |
+            ((Lhz0 & Lhqm) << 5) | ((nz0 & (uint32_t)hqm) << 6) | ((Lhz0 & (Lhq0 ^ 1u)) << 7) |
+            ((nz0 & (uint32_t)!hq0) << 8);
+    };
+
+    tour::Plane<tour::NB3> cur, nxt;
+    T vcur = T(0), vnxt = T(0);
+    plane(i0 - 1, nxt, vnxt);
+    plane(i0, cur, vcur);
+    uint32_t Xp = tour::xmask(cur, nxt);
+    for (int64_t i = i0; i < i1; ++i) {
+      plane(i + 1, nxt, vnxt);
+      const uint32_t X = tour::xmask(nxt, cur);
+      if (own) {
+        const int64_t vox = ((i - s.own0) * s.w1 + j) * s.w2 + k;
+        if constexpr (HIST) {
+          sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS3>(cur.I, X, Xp));
+        } else if constexpr (MODE == kChanges) {
+          static_cast<int8_t*>(out)[vox] = (int8_t)tour::change_of<tour::POS3>(cur.I, X, Xp);
+        } else {
+          static_cast<uint32_t*>(out)[vox] = tour::faces3(cur.I, X, Xp);
         }
+      }
+      Xp = X;
+      cur = nxt;
+      vcur = vnxt;
     }
   }
-  if constexpr (HIST) sink_flush<SMEM>(sink);
+  if constexpr (HIST) sink_flush(sink);
 }
 
 // ---------------------------------------------------------------- 2D
-// Stencil over axes 0 and 1 (w2 == 1, kernel.hpp:81-94).  1D block over j.
-template <class T, bool AFFINE, bool SMEM, bool HIST>
-__global__ void k_generic2(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
-                           uint32_t nbins, uint32_t* flags, int8_t* changes) {
+// Stencil over axes 0 and 1 (w2 == 1, kernel.hpp:81-94).  Block of 8 warps,
+// warp w of block b covers j = 30 * (8 b + w) + lane - 1.
+template <class T, bool AFFINE, int MODE>
+__global__ void __launch_bounds__(256) k_tour2(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
+                                               uint32_t nbins, uint32_t* flags, void* out) {
   extern __shared__ int32_t sh[];
-  HistSink<SMEM> sink;
-  if constexpr (HIST) sink_init<SMEM>(sink, ghist, nbins, sh);
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal;
+  HistSink<MODE == kHistSmem> sink;
+  if constexpr (HIST) sink_init(sink, ghist, nbins, sh);
+  constexpr uint32_t SENT = KeyTraits<T>::kSentinel;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * LANES_OWNED +
+                    lane - 1;
   const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
   const int64_t i1 = min(i0 + seg, s.own1);
-  if (j < s.w1 && i0 < i1) {
-    uint32_t w[3][3];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) w[a][b] = ldkey<T>(s, i0 - 1 + a, j - 1 + b, 0);
+  if (i0 < i1) {
+    const bool jin = j >= 0 && j < s.w1;
+    const bool own = jin && lane >= 1 && lane <= LANES_OWNED;
+    const int64_t pp = s.plane_pitch();
+    const T* ctr = static_cast<const T*>(s.base) + (jin ? j : 0) - s.plane0 * pp;
+    auto row = [&](int64_t i, tour::Plane<tour::NB2>& P, T& val) {
+      uint32_t a = SENT;
+      if (jin && i >= 0 && i < s.w0) {
+        val = __ldg(ctr + i * pp);
+        a = KeyTraits<T>::key(val);
+      }
+      const uint32_t b = __shfl_down_sync(FULLMASK, a, 1);  // j + 1
+      const uint32_t mb = min(a, b);
+      const bool hb = b < a;
+      const uint32_t Lmb = __shfl_up_sync(FULLMASK, mb, 1);   // pair anchored at j - 1
+      const uint32_t Lhb = __shfl_up_sync(FULLMASK, (uint32_t)hb, 1);
+      P.M[0] = a;
+      P.M[1] = Lmb;
+      P.M[2] = mb;
+      P.I = 1u | (Lhb << 1) | ((uint32_t)!hb << 2);
+    };
+    tour::Plane<tour::NB2> cur, nxt;
+    T vcur = T(0), vnxt = T(0);
+    row(i0 - 1, nxt, vnxt);
+    row(i0, cur, vcur);
+    uint32_t Xp = tour::xmask(cur, nxt);
     for (int64_t i = i0; i < i1; ++i) {
-#pragma unroll
-      for (int b = 0; b < 3; ++b) w[2][b] = ldkey<T>(s, i + 1, j - 1 + b, 0);
-      const int ch = change2(w);
-      if constexpr (HIST) {
-        const T v = ldval<T>(s, i, j, 0);
-        sink.add(bin_of<T, AFFINE>(v, am, flags), ch);
-      } else {
-        changes[(i - s.own0) * s.w1 + j] = static_cast<int8_t>(ch);
+      row(i + 1, nxt, vnxt);
+      const uint32_t X = tour::xmask(nxt, cur);
+      if (own) {
+        const int64_t vox = (i - s.own0) * s.w1 + j;
+        if constexpr (HIST) {
+          sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS2>(cur.I, X, Xp));
+        } else if constexpr (MODE == kChanges) {
+          static_cast<int8_t*>(out)[vox] = (int8_t)tour::change_of<tour::POS2>(cur.I, X, Xp);
+        } else {
+          static_cast<uint32_t*>(out)[vox] = tour::faces2(cur.I, X, Xp);
+        }
       }
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        w[0][b] = w[1][b];
-        w[1][b] = w[2][b];
-      }
+      Xp = X;
+      cur = nxt;
+      vcur = vnxt;
     }
   }
-  if constexpr (HIST) sink_flush<SMEM>(sink);
+  if constexpr (HIST) sink_flush(sink);
 }
 
 // ---------------------------------------------------------------- launch
@@ -199,37 +259,32 @@ namespace {
 
 constexpr uint32_t kSmemBinLimit = 8192;  // 2 x 8192 x 4 B = 64 KB
 
-template <class T, bool AFFINE, bool SMEM, bool HIST>
+template <class T, bool AFFINE, int MODE>
 cudaError_t launch_generic_t(const Slab& s, const AffineMap& am, int64_t* ghist,
-                             uint32_t nbins, uint32_t* flags, int8_t* changes,
-                             int sms, cudaStream_t st) {
+                             uint32_t nbins, uint32_t* flags, void* out, int sms,
+                             cudaStream_t st) {
   const int64_t owned = s.own1 - s.own0;
   const bool d3 = s.w2 > 1;
   dim3 block, grid;
-  int64_t cols;
   if (d3) {
     block = dim3(32, 8, 1);
-    grid = dim3((unsigned)((s.w2 + 31) / 32), (unsigned)((s.w1 + 7) / 8), 1);
+    grid = dim3((unsigned)((s.w2 + LANES_OWNED - 1) / LANES_OWNED), (unsigned)((s.w1 + 7) / 8), 1);
   } else {
     block = dim3(256, 1, 1);
-    grid = dim3((unsigned)((s.w1 + 255) / 256), 1, 1);
+    grid = dim3((unsigned)((s.w1 + 8 * LANES_OWNED - 1) / (8 * LANES_OWNED)), 1, 1);
   }
-  cols = (int64_t)grid.x * grid.y;
+  const int64_t cols = (int64_t)grid.x * grid.y;
   // enough CTAs for ~8 per SM, but segments of at least 8 planes
   int64_t nseg = (8LL * sms + cols - 1) / cols;
   nseg = std::max<int64_t>(1, std::min<int64_t>(nseg, (owned + 7) / 8));
   nseg = std::min<int64_t>(nseg, 65535);
   const int64_t seg = (owned + nseg - 1) / nseg;
   grid.z = (unsigned)((owned + seg - 1) / seg);
-  const size_t smem = (HIST && SMEM) ? 2 * nbins * sizeof(int32_t) : 0;
-  if (smem > 48 * 1024) {
-    auto fn = d3 ? k_generic3<T, AFFINE, SMEM, HIST> : k_generic2<T, AFFINE, SMEM, HIST>;
+  const size_t smem = MODE == kHistSmem ? 2 * nbins * sizeof(int32_t) : 0;
+  auto fn = d3 ? k_tour3<T, AFFINE, MODE> : k_tour2<T, AFFINE, MODE>;
+  if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  if (d3)
-    k_generic3<T, AFFINE, SMEM, HIST><<<grid, block, smem, st>>>(s, seg, am, ghist, nbins, flags, changes);
-  else
-    k_generic2<T, AFFINE, SMEM, HIST><<<grid, block, smem, st>>>(s, seg, am, ghist, nbins, flags, changes);
+  fn<<<grid, block, smem, st>>>(s, seg, am, ghist, nbins, flags, out);
   return cudaGetLastError();
 }
 
@@ -238,8 +293,22 @@ cudaError_t launch_generic_hist(const Slab& s, const AffineMap& am, int64_t* ghi
                                 uint32_t nbins, uint32_t* flags, int sms,
                                 cudaStream_t st) {
   if (nbins <= kSmemBinLimit)
-    return launch_generic_t<T, AFFINE, true, true>(s, am, ghist, nbins, flags, nullptr, sms, st);
-  return launch_generic_t<T, AFFINE, false, true>(s, am, ghist, nbins, flags, nullptr, sms, st);
+    return launch_generic_t<T, AFFINE, kHistSmem>(s, am, ghist, nbins, flags, nullptr, sms, st);
+  return launch_generic_t<T, AFFINE, kHistGlobal>(s, am, ghist, nbins, flags, nullptr, sms, st);
+}
+
+template <int MODE>
+cudaError_t launch_generic_out(const Slab& s, int dtype, void* out, int sms, cudaStream_t st) {
+  AffineMap am{};
+  switch (dtype) {
+    case 0:
+      return launch_generic_t<uint8_t, false, MODE>(s, am, nullptr, 0, nullptr, out, sms, st);
+    case 1:
+      return launch_generic_t<uint16_t, false, MODE>(s, am, nullptr, 0, nullptr, out, sms, st);
+    case 2:
+      return launch_generic_t<float, false, MODE>(s, am, nullptr, 0, nullptr, out, sms, st);
+  }
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace
@@ -262,16 +331,12 @@ cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
 
 cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sms,
                                    cudaStream_t st) {
-  AffineMap am{};
-  switch (dtype) {
-    case 0:
-      return launch_generic_t<uint8_t, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
-    case 1:
-      return launch_generic_t<uint16_t, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
-    case 2:
-      return launch_generic_t<float, false, false, false>(s, am, nullptr, 0, nullptr, out, sms, st);
-  }
-  return cudaErrorInvalidValue;
+  return launch_generic_out<kChanges>(s, dtype, out, sms, st);
+}
+
+cudaError_t launch_generic_faces(const Slab& s, int dtype, uint32_t* out, int sms,
+                                 cudaStream_t st) {
+  return launch_generic_out<kFaces>(s, dtype, out, sms, st);
 }
 
 // ---------------------------------------------------------------- order keys
