@@ -136,6 +136,41 @@ int read_rows_tramp(void* user, std::uint64_t r0, std::uint64_t r1, void* dst, c
 
 }  // namespace detail
 
+// EngineReport from the per-chunk timings: phase sums and the bytes of the
+// pinned staging the driver holds (two buffers of the largest chunk's rows
+// plus its halo rows -- the GPU counterpart of the reference's <= 2 resident
+// padded chunks, and what is registered with chunk_memory()).
+inline std::uint64_t staging_bytes(const ChunkPlan& plan, const Dims& dims, std::size_t elem) {
+  std::uint64_t rows = 0;
+  for (const auto& r : plan.ranges) rows = std::max(rows, r.len() + 2);
+  return 2 * std::min(rows, dims.w0) * dims.w1 * dims.w2 * elem;
+}
+
+inline void fill_report(EngineReport* report, const std::vector<ecc_chunk_timing>& tim,
+                        std::uint64_t staging) {
+  if (!report) return;
+  report->chunks.clear();
+  report->read_s = report->index_s = report->kernel_s = report->merge_s = 0;
+  for (const auto& t : tim) {
+    ChunkTiming c;
+    c.range = {t.begin, t.end};
+    c.ingest_begin = t.ingest_begin;
+    c.ingest_end = t.ingest_end;
+    c.index_begin = t.index_begin;
+    c.index_end = t.index_end;
+    c.kernel_begin = t.kernel_begin;
+    c.kernel_end = t.kernel_end;
+    c.merge_begin = t.merge_begin;
+    c.merge_end = t.merge_end;
+    report->read_s += c.ingest_end - c.ingest_begin;
+    report->index_s += c.index_end - c.index_begin;
+    report->kernel_s += c.kernel_end - c.kernel_begin;
+    report->merge_s += c.merge_end - c.merge_begin;
+    report->chunks.push_back(c);
+  }
+  report->peak_chunk_bytes = staging;
+}
+
 template <class T>
 GlobalVcec<T> process_image(ChunkSource<T>& source, const ChunkPlan& plan,
                             const EngineOptions& opt = {}, EngineReport* report = nullptr) {
@@ -162,6 +197,8 @@ GlobalVcec<T> process_image(ChunkSource<T>& source, const ChunkPlan& plan,
   else
     detail::check(ecc_bin_count(detail::dtype_of<T>::value, pb, &cap));
   std::vector<ecc_chunk_timing> tim(plan.ranges.size());
+  const std::uint64_t staging = staging_bytes(plan, dims, sizeof(T));
+  const TrackedBytes held(staging);
   for (;;) {
     GlobalVcec<T> out;
     out.values.resize(cap);
@@ -179,30 +216,7 @@ GlobalVcec<T> process_image(ChunkSource<T>& source, const ChunkPlan& plan,
     detail::check(rc);
     out.values.resize(n);
     out.changes.resize(n);
-    if (report) {
-      report->chunks.clear();
-      report->read_s = report->index_s = report->kernel_s = report->merge_s = 0;
-      for (const auto& t : tim) {
-        ChunkTiming c;
-        c.range = {t.begin, t.end};
-        c.ingest_begin = t.ingest_begin;
-        c.ingest_end = t.ingest_end;
-        c.index_begin = t.index_begin;
-        c.index_end = t.index_end;
-        c.kernel_begin = t.kernel_begin;
-        c.kernel_end = t.kernel_end;
-        c.merge_begin = t.merge_begin;
-        c.merge_end = t.merge_end;
-        report->read_s += c.ingest_end - c.ingest_begin;
-        report->index_s += c.index_end - c.index_begin;
-        report->kernel_s += c.kernel_end - c.kernel_begin;
-        report->merge_s += c.merge_end - c.merge_begin;
-        report->chunks.push_back(c);
-      }
-      std::uint64_t rows = 0;
-      for (const auto& r : plan.ranges) rows = std::max(rows, r.len() + 2);
-      report->peak_chunk_bytes = 2 * std::min(rows, dims.w0) * dims.w1 * dims.w2 * sizeof(T);
-    }
+    fill_report(report, tim, staging);
     return out;
   }
 }
@@ -227,6 +241,8 @@ GlobalVcec<T> process_image(FileSource<T>& source, const ChunkPlan& plan,
   else
     detail::check(ecc_bin_count(detail::dtype_of<T>::value, pb, &cap));
   std::vector<ecc_chunk_timing> tim(plan.ranges.size());
+  const std::uint64_t staging = staging_bytes(plan, dims, sizeof(T));
+  const TrackedBytes held(staging);
   for (;;) {
     GlobalVcec<T> out;
     out.values.resize(cap);
@@ -243,13 +259,7 @@ GlobalVcec<T> process_image(FileSource<T>& source, const ChunkPlan& plan,
     detail::check(rc);
     out.values.resize(n);
     out.changes.resize(n);
-    if (report) {
-      report->chunks.clear();
-      for (const auto& t : tim)
-        report->chunks.push_back({{t.begin, t.end}, t.ingest_begin, t.ingest_end, t.index_begin,
-                                  t.index_end, t.kernel_begin, t.kernel_end, t.merge_begin,
-                                  t.merge_end});
-    }
+    fill_report(report, tim, staging);
     return out;
   }
 }

@@ -314,6 +314,88 @@ ECC_API int ecc_gaussian_smooth(ecc_ctx* ctx, const float* d_in, float* d_out, e
 ECC_API int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t seed,
                           double sigma, int width, ecc_bench_report* report);
 
+/* ------------------------------------------------------------ L1/L2: padded chunks
+ * The reference's chunk-level API (kernel.hpp:32-74, 229-277,
+ * value_index.hpp:23-197, vcec.hpp:35-66) on the device.  `padded` is a
+ * PaddedChunk's host storage (chunk.hpp:50-127): (len+2) x (w1+2) x (w2+2)
+ * extended values -- int16 for u8 (sentinel 256), int32 for u16 (65536),
+ * float for f32 (+inf) -- with the one-voxel collar and the padding rows
+ * begin-1 / end, len = end - begin.  The device evaluates the stencil on
+ * exactly the stored values (collar and padding rows included), so a chunk
+ * built by hand with set_padded behaves as in the reference.  Rows
+ * [row_begin, row_end) are relative to the chunk (0 = row `begin`).  Host
+ * outputs; synchronous. */
+typedef struct {
+  ecc_dims image;      /* the image the chunk belongs to */
+  uint64_t begin, end; /* owned rows [begin, end) along axis 0 */
+} ecc_chunk;
+
+/* Per-voxel Euler changes of the owned voxels of rows [row_begin, row_end),
+ * owned row-major order (compute_changes, kernel.hpp:244-265). */
+ECC_API int ecc_chunk_changes(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                              uint64_t row_begin, uint64_t row_end, int8_t* out);
+
+/* Per owned voxel, the FaceOffsets o it introduces (introduced(),
+ * kernel.hpp:32-53): bit (o0+1)*9 + (o1+1)*3 + (o2+1), bit 13 never set.
+ * 2D chunks are evaluated over their padded axis 2 as well, so offsets with
+ * o2 != 0 meet the collar exactly as in the reference. */
+ECC_API int ecc_chunk_faces(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                            uint64_t row_begin, uint64_t row_end, uint32_t* out);
+
+/* Change sums per bin over the owned voxels of rows [row_begin, row_end):
+ * index_values == NULL -> identity bins of the (narrowed) value, nbins = 256
+ * (u8; accumulate_dense_u8, kernel.hpp:268-277) or 65536 (u16); otherwise the
+ * bins of a value index (ValueIndex<float>, value_index.hpp:23-58): bin b is
+ * index_values[b] (ascending, distinct, nbins of them) and every voxel value
+ * must be one of them (accumulate_chunk, kernel.hpp:229-239; else
+ * ECC_EBINMAP "value not present in index").  hist_out: nbins int64. */
+ECC_API int ecc_chunk_accumulate(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                                 uint64_t row_begin, uint64_t row_end, const float* index_values,
+                                 uint64_t nbins, int64_t* hist_out);
+
+/* The occurring values of `values` (n elements of dtype, host), ascending and
+ * distinct (f32: -0 folds onto +0, NaN -> ECC_ENAN "cannot build a value
+ * index: NaN input"), and -- when `changes` (n int8, host) is given -- the
+ * summed change of each (ValueIndex::build value_index.hpp:23-71,
+ * build_index_counts :159-197: device radix sort + reduce-by-key).
+ * values_out / sums_out: host, capacity cap; *n_out = distinct count (also
+ * when it exceeds cap, with ECC_EINVAL). */
+ECC_API int ecc_value_index(ecc_ctx* ctx, ecc_dtype dtype, const void* values, uint64_t n,
+                            const int8_t* changes, void* values_out, int64_t* sums_out,
+                            uint64_t cap, uint64_t* n_out);
+
+/* Same over the owned voxels of a padded chunk (build_index_counts on its
+ * owned voxels in owned row-major order, changes as compute_changes wrote
+ * them). */
+ECC_API int ecc_chunk_index_counts(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                                   const int8_t* changes, void* values_out, int64_t* sums_out,
+                                   uint64_t cap, uint64_t* n_out);
+
+/* merge_local (vcec.hpp:35-66) on the device: the global VCEC (gvals /
+ * gchg, gn entries, ascending) plus, for every occurring value ivals[i] of a
+ * chunk index (in entries, ascending), local[bin] where bin = the value for
+ * u8 / u16 and i for f32; values new to the global list are inserted (zero
+ * changes included).  Host arrays; out_* capacity cap (gn + in suffices). */
+ECC_API int ecc_merge_local(ecc_ctx* ctx, ecc_dtype dtype, const void* gvals,
+                            const int64_t* gchg, uint64_t gn, const int64_t* local,
+                            uint64_t nlocal, const void* ivals, uint64_t in, void* out_vals,
+                            int64_t* out_chg, uint64_t cap, uint64_t* n_out);
+
+/* ------------------------------------------------------------ host-buffer helpers
+ * The reference's host-facing generators and raw-file fixup with host arrays
+ * in and out; the work runs on the device (the C++ headers' datagen.hpp,
+ * image.hpp, FileSource::read_rows).  Synchronous.
+ * ecc_uniform_noise_host: uniform_noise (datagen.hpp:57-62) into host memory.
+ * ecc_gaussian_smooth_host: gaussian_smooth (datagen.hpp:108-122); in may equal out.
+ * ecc_fixup_f32_host: fixup_loaded (image.hpp:39-52) in place: byte swap when
+ *   big_endian, then ECC_ENAN "NaN value at linear index <base + i>" for the
+ *   first NaN. */
+ECC_API int ecc_uniform_noise_host(ecc_ctx* ctx, float* out, uint64_t n, uint64_t seed);
+ECC_API int ecc_gaussian_smooth_host(ecc_ctx* ctx, const float* in, float* out, ecc_dims dims,
+                                     double sigma, int width);
+ECC_API int ecc_fixup_f32_host(ecc_ctx* ctx, float* data, uint64_t n, uint64_t base,
+                               int big_endian);
+
 #ifdef __cplusplus
 }
 #endif

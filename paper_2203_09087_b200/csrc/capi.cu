@@ -1953,3 +1953,377 @@ int ecc_curve_sharded(ecc_ctx* ctx, ecc_xchg* x, const void* d_planes, ecc_dims 
 }
 
 }  // extern "C"
+
+// ===================================================================== padded chunks
+// The reference's chunk-level API on the device (ecc_chunk_*, ecc_value_index,
+// ecc_merge_local; see ecc_b200.h).  The PaddedChunk storage is uploaded as
+// is and turned into a key image (k_chunk_keys), so the stencil sees exactly
+// the stored extended values, collar and padding rows included.
+namespace {
+
+size_t ext_size(ecc_dtype t) { return t == ECC_U8 ? 2 : 4; }
+int ext_type(ecc_dtype t) { return t == ECC_U8 ? 0 : (t == ECC_U16 ? 1 : 2); }
+
+int check_chunk(const ecc_chunk& c, uint64_t r0, uint64_t r1) {
+  CKI(check_dims(c.image));
+  if (!(c.begin < c.end) || c.end > c.image.w0)
+    return fail(ECC_EINVAL, "invalid chunk range [" + std::to_string(c.begin) + ", " +
+                                std::to_string(c.end) + ") for dims " + dims_str(c.image));
+  if (r0 > r1 || r1 > c.end - c.begin)
+    return fail(ECC_EINVAL, "rows [" + std::to_string(r0) + ", " + std::to_string(r1) +
+                                ") are outside the chunk's " + std::to_string(c.end - c.begin) +
+                                " owned rows");
+  return ECC_OK;
+}
+
+// Padded rows [r0, r1 + 2) -> key image in ctx->keys; *s describes it with
+// owned rows r0..r1-1 (key-image planes 1..np-2) and the collar not owned.
+// as3d: evaluate a 2D chunk with the 3D stencil over its padded axis 2 (the
+// reference's introduced() is dimension-free: offsets along axis 2 meet the
+// collar).
+int chunk_keyimage(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, const ecc_chunk& c,
+                   uint64_t r0, uint64_t r1, cudaStream_t st, Slab* s, bool as3d = false) {
+  const bool is2d = c.image.w2 == 1 && !as3d;
+  const uint64_t w1p = c.image.w1 + 2, w2p = c.image.w2 + 2, plane = w1p * w2p;
+  const uint64_t np = r1 - r0 + 2;
+  const size_t es = ext_size(dtype);
+  CKI(ctx->input.ensure(np * plane * es));
+  CKR(cudaMemcpyAsync(ctx->input.p, static_cast<const char*>(padded) + r0 * plane * es,
+                      np * plane * es, cudaMemcpyHostToDevice, st));
+  const uint64_t w2k = is2d ? 1 : w2p;
+  CKI(ctx->keys.ensure(np * w1p * w2k * 4));
+  CKR(launch_chunk_keys(ctx->input.p, ext_type(dtype), np, w1p, w2p, is2d, false,
+                        ctx->keys.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 1;
+  Slab k{};
+  k.base = ctx->keys.p;
+  k.plane0 = 0;
+  k.nplanes = (int64_t)np;
+  k.w0 = (int64_t)np;
+  k.w1 = (int64_t)w1p;
+  k.w2 = (int64_t)w2k;
+  k.own0 = 1;
+  k.own1 = (int64_t)np - 1;
+  k.oj0 = 1;
+  k.oj1 = (int64_t)w1p - 1;
+  if (!is2d) {
+    k.ok0 = 1;
+    k.ok1 = (int64_t)w2p - 1;
+  }
+  *s = k;
+  return ECC_OK;
+}
+
+int check_ptr(const void* p, const char* what) {
+  if (!p) return fail(ECC_EINVAL, std::string("null ") + what);
+  return ECC_OK;
+}
+
+// Sort + reduce-by-key of (ctx->keys2[0..n), ctx->ch8[0..n)) into
+// (ctx->akeys, ctx->asums); *m = distinct keys.
+int reduce_keys(ecc_ctx* ctx, uint64_t n, cudaStream_t st, uint64_t* m) {
+  if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "value list exceeds 2^31 entries");
+  CKI(ctx->keys.ensure(n * 4));
+  CKI(ctx->ch8b.ensure(n));
+  CKI(ctx->akeys.ensure(n * 4));
+  CKI(ctx->asums.ensure(n * 8));
+  CKI(ctx->count.ensure(8));
+  size_t t1 = 0, t2 = 0;
+  auto vals = thrust::make_transform_iterator(ctx->ch8b.as<const int8_t>(), ToI64());
+  CKR(cub::DeviceRadixSort::SortPairs(nullptr, t1, ctx->keys2.as<uint32_t>(), ctx->keys.as<uint32_t>(),
+                                      ctx->ch8.as<int8_t>(), ctx->ch8b.as<int8_t>(), (int)n, 0, 32,
+                                      st));
+  CKR(cub::DeviceReduce::ReduceByKey(nullptr, t2, ctx->keys.as<uint32_t>(), ctx->akeys.as<uint32_t>(),
+                                     vals, ctx->asums.as<int64_t>(), ctx->count.as<uint64_t>(),
+                                     cub::Sum(), (int)n, st));
+  CKI(ctx->tmp.ensure(std::max(t1, t2)));
+  t1 = ctx->tmp.cap;
+  CKR(cub::DeviceRadixSort::SortPairs(ctx->tmp.p, t1, ctx->keys2.as<uint32_t>(),
+                                      ctx->keys.as<uint32_t>(), ctx->ch8.as<int8_t>(),
+                                      ctx->ch8b.as<int8_t>(), (int)n, 0, 32, st));
+  t2 = ctx->tmp.cap;
+  CKR(cub::DeviceReduce::ReduceByKey(ctx->tmp.p, t2, ctx->keys.as<uint32_t>(),
+                                     ctx->akeys.as<uint32_t>(), vals, ctx->asums.as<int64_t>(),
+                                     ctx->count.as<uint64_t>(), cub::Sum(), (int)n, st));
+  ctx->launches += 2;
+  CKR(cudaMemcpyAsync(m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+// (akeys, asums)[0..m) -> host values of dtype (keys decoded by `decode`) and sums.
+int emit_keys(ecc_ctx* ctx, ecc_dtype dtype, uint64_t m, int decode, void* values_out,
+              int64_t* sums_out, uint64_t cap, uint64_t* n_out, cudaStream_t st) {
+  *n_out = m;
+  if (m > cap) return fail(ECC_EINVAL, "output capacity " + std::to_string(cap) + " < " +
+                                           std::to_string(m) + " distinct values");
+  std::vector<uint32_t> keys(m);
+  if (m) CKR(cudaMemcpyAsync(keys.data(), ctx->akeys.p, m * 4, cudaMemcpyDeviceToHost, st));
+  if (m && sums_out)
+    CKR(cudaMemcpyAsync(sums_out, ctx->asums.p, m * 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  for (uint64_t i = 0; i < m; ++i) {
+    uint32_t k = keys[i];
+    if (decode == 1) k -= 32768u;            // int16 extended u8
+    else if (decode == 2) k ^= 0x80000000u;  // int32 extended u16
+    if (dtype == ECC_U8) static_cast<uint8_t*>(values_out)[i] = (uint8_t)k;
+    else if (dtype == ECC_U16) static_cast<uint16_t*>(values_out)[i] = (uint16_t)k;
+    else static_cast<float*>(values_out)[i] = key_to_float(k);
+  }
+  return ECC_OK;
+}
+
+int read_flag_errors(ecc_ctx* ctx, cudaStream_t st, const char* binmap_msg) {
+  uint32_t f = 0;
+  CKR(cudaMemcpyAsync(&f, ctx->flags.p, 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  if (f & kFlagNaN) return fail(ECC_ENAN, "cannot build a value index: NaN input");
+  if (f & kFlagBinmap) return fail(ECC_EBINMAP, binmap_msg);
+  return ECC_OK;
+}
+
+}  // namespace
+
+int ecc_chunk_changes(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                      uint64_t row_begin, uint64_t row_end, int8_t* out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(padded, "padded chunk"));
+  CKI(check_chunk(c, row_begin, row_end));
+  const uint64_t n = (row_end - row_begin) * c.image.w1 * c.image.w2;
+  if (n == 0) return ECC_OK;
+  CKI(check_ptr(out, "output"));
+  cudaStream_t st = ctx->stream;
+  Slab s;
+  CKI(chunk_keyimage(ctx, padded, dtype, c, row_begin, row_end, st, &s));
+  CKI(ctx->ch8.ensure(n));
+  AffineMap am{};
+  CKR(launch_keyimage(s, 2, am, nullptr, 0, nullptr, ctx->ch8.p, ctx->sms, st));
+  ctx->launches += 1;
+  CKR(cudaMemcpyAsync(out, ctx->ch8.p, n, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_chunk_faces(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                    uint64_t row_begin, uint64_t row_end, uint32_t* out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(padded, "padded chunk"));
+  CKI(check_chunk(c, row_begin, row_end));
+  const uint64_t n = (row_end - row_begin) * c.image.w1 * c.image.w2;
+  if (n == 0) return ECC_OK;
+  CKI(check_ptr(out, "output"));
+  cudaStream_t st = ctx->stream;
+  Slab s;
+  CKI(chunk_keyimage(ctx, padded, dtype, c, row_begin, row_end, st, &s, true));
+  CKI(ctx->keys2.ensure(n * 4));
+  AffineMap am{};
+  CKR(launch_keyimage(s, 3, am, nullptr, 0, nullptr, ctx->keys2.p, ctx->sms, st));
+  ctx->launches += 1;
+  CKR(cudaMemcpyAsync(out, ctx->keys2.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_chunk_accumulate(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                         uint64_t row_begin, uint64_t row_end, const float* index_values,
+                         uint64_t nbins, int64_t* hist_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(padded, "padded chunk"));
+  CKI(check_ptr(hist_out, "histogram"));
+  CKI(check_chunk(c, row_begin, row_end));
+  AffineMap am{};
+  if (!index_values) {
+    if (dtype == ECC_F32) return fail(ECC_EINVAL, "f32 chunks are binned by a value index");
+    const uint64_t want = dtype == ECC_U8 ? 256 : 65536;
+    if (nbins != want)
+      return fail(ECC_EINVAL, "identity bins of this dtype number " + std::to_string(want));
+    am.key_lo = dtype == ECC_U8 ? 32768u : 0x80000000u;  // the key image's encoding
+    am.key_mask = (uint32_t)(want - 1);
+  } else {
+    if (nbins == 0 || nbins > 0x7FFFFFFFull)
+      return fail(ECC_EINVAL, "a value index needs 1 .. 2^31 bins");
+  }
+  std::fill(hist_out, hist_out + nbins, 0);
+  if (row_begin == row_end) return ECC_OK;
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->flags.ensure(16));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 16, st));
+  if (index_values) {
+    // the table in key space: order keys of the index values (value_index.hpp:95-99)
+    CKI(ctx->bins.ensure(nbins * 4));
+    CKI(ctx->sums2.ensure(nbins * 4));
+    CKR(cudaMemcpyAsync(ctx->sums2.p, index_values, nbins * 4, cudaMemcpyHostToDevice, st));
+    CKR(launch_value_keys(ctx->sums2.p, (int)ECC_F32, nbins, ctx->bins.as<uint32_t>(),
+                          ctx->flags.as<uint32_t>(), ctx->sms, st));
+    ctx->launches += 1;
+    am.table = ctx->bins.as<uint32_t>();
+    am.table_n = (uint32_t)nbins;
+  }
+  Slab s;
+  CKI(chunk_keyimage(ctx, padded, dtype, c, row_begin, row_end, st, &s));
+  CKI(ctx->hist.ensure(2 * nbins * 8));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * nbins * 8, st));
+  CKR(launch_keyimage(s, 0, am, ctx->hist.as<int64_t>(), (uint32_t)nbins,
+                      ctx->flags.as<uint32_t>(), nullptr, ctx->sms, st));
+  ctx->launches += 1;
+  CKI(read_flag_errors(ctx, st, "value not present in index (internal consistency bug)"));
+  CKR(cudaMemcpyAsync(hist_out, ctx->hist.p, nbins * 8, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_value_index(ecc_ctx* ctx, ecc_dtype dtype, const void* values, uint64_t n,
+                    const int8_t* changes, void* values_out, int64_t* sums_out, uint64_t cap,
+                    uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(n_out, "count output"));
+  *n_out = 0;
+  if (n == 0) return fail(ECC_EINVAL, "cannot build a value index: empty input");
+  CKI(check_ptr(values, "values"));
+  CKI(check_ptr(values_out, "values output"));
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->flags.ensure(16));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 16, st));
+  CKI(ctx->input.ensure(n * esize(dtype)));
+  CKR(cudaMemcpyAsync(ctx->input.p, values, n * esize(dtype), cudaMemcpyHostToDevice, st));
+  CKI(ctx->keys2.ensure(n * 4));
+  CKI(ctx->ch8.ensure(n));
+  CKR(launch_value_keys(ctx->input.p, (int)dtype, n, ctx->keys2.as<uint32_t>(),
+                        ctx->flags.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 1;
+  if (changes) CKR(cudaMemcpyAsync(ctx->ch8.p, changes, n, cudaMemcpyHostToDevice, st));
+  else CKR(cudaMemsetAsync(ctx->ch8.p, 0, n, st));
+  CKI(read_flag_errors(ctx, st, "value not present in index"));
+  uint64_t m = 0;
+  CKI(reduce_keys(ctx, n, st, &m));
+  return emit_keys(ctx, dtype, m, 0, values_out, changes ? sums_out : nullptr, cap, n_out, st);
+}
+
+int ecc_chunk_index_counts(ecc_ctx* ctx, const void* padded, ecc_dtype dtype, ecc_chunk c,
+                           const int8_t* changes, void* values_out, int64_t* sums_out,
+                           uint64_t cap, uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(padded, "padded chunk"));
+  CKI(check_ptr(n_out, "count output"));
+  CKI(check_ptr(values_out, "values output"));
+  *n_out = 0;
+  CKI(check_chunk(c, 0, c.end - c.begin));
+  const bool is2d = c.image.w2 == 1;
+  const uint64_t len = c.end - c.begin, w1p = c.image.w1 + 2, w2p = c.image.w2 + 2;
+  const uint64_t n = len * c.image.w1 * c.image.w2;
+  if (n > 0xFFFFFFFFull) return fail(ECC_EINVAL, "chunk exceeds 2^32 voxels; use a finer chunk plan");
+  cudaStream_t st = ctx->stream;
+  const size_t es = ext_size(dtype);
+  CKI(ctx->input.ensure((len + 2) * w1p * w2p * es));
+  CKR(cudaMemcpyAsync(ctx->input.p, padded, (len + 2) * w1p * w2p * es, cudaMemcpyHostToDevice, st));
+  CKI(ctx->keys2.ensure(n * 4));
+  CKI(ctx->ch8.ensure(n));
+  CKR(launch_chunk_keys(ctx->input.p, ext_type(dtype), len + 2, w1p, w2p, is2d, true,
+                        ctx->keys2.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 1;
+  if (changes) CKR(cudaMemcpyAsync(ctx->ch8.p, changes, n, cudaMemcpyHostToDevice, st));
+  else CKR(cudaMemsetAsync(ctx->ch8.p, 0, n, st));
+  uint64_t m = 0;
+  CKI(reduce_keys(ctx, n, st, &m));
+  const int decode = dtype == ECC_U8 ? 1 : (dtype == ECC_U16 ? 2 : 0);
+  return emit_keys(ctx, dtype, m, decode, values_out, changes ? sums_out : nullptr, cap, n_out, st);
+}
+
+int ecc_merge_local(ecc_ctx* ctx, ecc_dtype dtype, const void* gvals, const int64_t* gchg,
+                    uint64_t gn, const int64_t* local, uint64_t nlocal, const void* ivals,
+                    uint64_t in, void* out_vals, int64_t* out_chg, uint64_t cap,
+                    uint64_t* n_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  CKI(check_ptr(n_out, "count output"));
+  *n_out = 0;
+  if ((gn && (!gvals || !gchg)) || (in && (!ivals || !local)) || !out_vals || !out_chg)
+    return fail(ECC_EINVAL, "null merge_local argument");
+  const uint64_t want = dtype == ECC_U8 ? 256 : (dtype == ECC_U16 ? 65536 : in);
+  if (nlocal != want)
+    return fail(ECC_EINVAL, "local VCEC length does not match the index bin count");
+  const uint64_t n = gn + in;
+  if (n == 0) return ECC_OK;
+  if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "too many distinct values to merge");
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->flags.ensure(16));
+  CKR(cudaMemsetAsync(ctx->flags.p, 0, 16, st));
+  const size_t es = esize(dtype);
+  CKI(ctx->input.ensure(n * es));
+  CKI(ctx->akeys.ensure(n * 4));
+  CKI(ctx->asums.ensure(n * 8));
+  CKI(ctx->sums.ensure(std::max<uint64_t>(nlocal, 1) * 8));
+  if (gn) {
+    CKR(cudaMemcpyAsync(ctx->input.p, gvals, gn * es, cudaMemcpyHostToDevice, st));
+    CKR(cudaMemcpyAsync(ctx->asums.p, gchg, gn * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (in) {
+    CKR(cudaMemcpyAsync(ctx->input.as<uint8_t>() + gn * es, ivals, in * es, cudaMemcpyHostToDevice,
+                        st));
+    CKR(cudaMemcpyAsync(ctx->sums.p, local, nlocal * 8, cudaMemcpyHostToDevice, st));
+  }
+  CKR(launch_value_keys(ctx->input.p, (int)dtype, n, ctx->akeys.as<uint32_t>(),
+                        ctx->flags.as<uint32_t>(), ctx->sms, st));
+  CKR(launch_gather_local(ctx->akeys.as<uint32_t>() + gn, dtype != ECC_F32, in,
+                          ctx->sums.as<int64_t>(), nlocal, ctx->asums.as<int64_t>() + gn,
+                          ctx->flags.as<uint32_t>(), ctx->sms, st));
+  ctx->launches += 2;
+  CKI(read_flag_errors(ctx, st, "value not present in index (internal consistency bug)"));
+  uint64_t m = 0;
+  CKI(merge_runs(ctx, st, n, &m));
+  return emit_keys(ctx, dtype, m, 0, out_vals, out_chg, cap, n_out, st);
+}
+
+// ===================================================================== host-buffer helpers
+int ecc_uniform_noise_host(ecc_ctx* ctx, float* out, uint64_t n, uint64_t seed) {
+  CKI(bind(ctx));
+  if (n == 0) return ECC_OK;
+  if (!out) return fail(ECC_EINVAL, "null output");
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->input.ensure(n * 4));
+  CKR(launch_uniform_noise(ctx->input.as<float>(), n, seed, ctx->sms, st));
+  ctx->launches += 1;
+  CKR(cudaMemcpyAsync(out, ctx->input.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_gaussian_smooth_host(ecc_ctx* ctx, const float* in, float* out, ecc_dims dims,
+                             double sigma, int width) {
+  CKI(bind(ctx));
+  CKI(check_dims(dims));
+  if (!in || !out) return fail(ECC_EINVAL, "null host pointer");
+  cudaStream_t st = ctx->stream;
+  const uint64_t n = dims.w0 * dims.w1 * dims.w2;
+  CKI(ctx->input.ensure(n * 4));
+  CKR(cudaMemcpyAsync(ctx->input.p, in, n * 4, cudaMemcpyHostToDevice, st));
+  CKI(smooth_device(ctx, ctx->input.as<float>(), ctx->input.as<float>(), dims, sigma, width, st));
+  CKR(cudaMemcpyAsync(out, ctx->input.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  return ECC_OK;
+}
+
+int ecc_fixup_f32_host(ecc_ctx* ctx, float* data, uint64_t n, uint64_t base, int big_endian) {
+  CKI(bind(ctx));
+  if (n == 0) return ECC_OK;
+  if (!data) return fail(ECC_EINVAL, "null host pointer");
+  cudaStream_t st = ctx->stream;
+  CKI(ctx->input.ensure(n * 4));
+  CKI(ctx->nanidx.ensure(8));
+  CKR(cudaMemsetAsync(ctx->nanidx.p, 0xFF, 8, st));
+  CKR(cudaMemcpyAsync(ctx->input.p, data, n * 4, cudaMemcpyHostToDevice, st));
+  CKR(launch_fixup(ctx->input.p, ECC_F32, n, base, big_endian != 0,
+                   ctx->nanidx.as<unsigned long long>(), ctx->sms, st));
+  ctx->launches += 1;
+  unsigned long long first = ~0ull;
+  CKR(cudaMemcpyAsync(&first, ctx->nanidx.p, 8, cudaMemcpyDeviceToHost, st));
+  if (big_endian) CKR(cudaMemcpyAsync(data, ctx->input.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CKR(cudaStreamSynchronize(st));
+  if (first != ~0ull) return fail(ECC_ENAN, "NaN value at linear index " + std::to_string(first));
+  return ECC_OK;
+}

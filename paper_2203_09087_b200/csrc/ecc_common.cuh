@@ -23,6 +23,14 @@ struct KeyTraits<uint8_t> {
   __device__ __forceinline__ static uint32_t key(uint8_t v) { return v; }
 };
 
+// Key images (the device copy of a PaddedChunk, ecc_chunk_*): the values are
+// already order-preserving keys; the sentinel beyond the image is above them.
+template <>
+struct KeyTraits<uint32_t> {
+  static constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+  __device__ __forceinline__ static uint32_t key(uint32_t v) { return v; }
+};
+
 template <>
 struct KeyTraits<uint16_t> {
   static constexpr uint32_t kSentinel = 65536u;
@@ -66,6 +74,8 @@ struct AffineMap {
   // must hold it exactly (else ECC_EBINMAP)
   const uint32_t* table = nullptr;
   uint32_t table_n = 0;
+  // key images without a table: bin = (key - key_lo) & key_mask
+  uint32_t key_mask = 0xFFFFFFFFu;
 };
 
 __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,
@@ -116,6 +126,11 @@ struct Slab {
   int64_t own0, own1;
   int64_t pitch = 0;  // elements between consecutive rows in memory (0 = w2)
   int64_t ppitch = 0; // elements between consecutive planes (0 = w1 * row_pitch())
+  // owned box along axes 1 and 2 (generic kernels only; -1 = the full axis):
+  // a PaddedChunk's collar is part of the device image but owns no voxels
+  int64_t oj0 = 0, oj1 = -1, ok0 = 0, ok1 = -1;
+  __host__ __device__ int64_t own_j1() const { return oj1 < 0 ? w1 : oj1; }
+  __host__ __device__ int64_t own_k1() const { return ok1 < 0 ? w2 : ok1; }
   __host__ __device__ int64_t row_pitch() const { return pitch ? pitch : w2; }
   __host__ __device__ int64_t plane_pitch() const { return ppitch ? ppitch : w1 * row_pitch(); }
 };

@@ -63,6 +63,18 @@ cudaError_t launch_generic_accumulate(const Slab& s, int dtype, bool affine,
                                       cudaStream_t st);
 cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sms,
                                    cudaStream_t st);
+// PaddedChunk storage -> uint32 key image (etype 0 int16, 1 int32, 2 float)
+cudaError_t launch_chunk_keys(const void* padded, int etype, uint64_t np, uint64_t w1p,
+                              uint64_t w2p, bool is2d, bool interior, uint32_t* keys, int sms,
+                              cudaStream_t st);
+// generic kernels over a key image; mode 0 histogram, 2 changes, 3 faces
+cudaError_t launch_keyimage(const Slab& s, int mode, const AffineMap& am, int64_t* ghist,
+                            uint32_t nbins, uint32_t* flags, void* out, int sms, cudaStream_t st);
+cudaError_t launch_value_keys(const void* v, int dtype, uint64_t n, uint32_t* keys,
+                              uint32_t* flags, int sms, cudaStream_t st);
+cudaError_t launch_gather_local(const uint32_t* keys, bool by_value, uint64_t n,
+                                const int64_t* local, uint64_t nlocal, int64_t* sums,
+                                uint32_t* flags, int sms, cudaStream_t st);
 // per owned voxel, the mask of FaceOffsets it introduces (tourney.cuh faces3)
 cudaError_t launch_generic_faces(const Slab& s, int dtype, uint32_t* out, int sms,
                                  cudaStream_t st);

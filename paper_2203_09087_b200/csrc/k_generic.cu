@@ -11,6 +11,8 @@
 // warp-shuffled neighbours, nine minimum-vs-minimum comparisons along axis 0
 // and two popcounts.  Lanes 0 and 31 of a warp are halo (their keys feed the
 // neighbouring lanes' blocks); lanes 1..30 own voxels.
+#include <type_traits>
+
 #include <cub/cub.cuh>
 
 #include "ecc_common.cuh"
@@ -21,7 +23,19 @@ namespace eccb {
 
 template <class T, bool AFFINE>
 __device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am, uint32_t* flags) {
-  if constexpr (AFFINE) {
+  if constexpr (std::is_same_v<T, uint32_t>) {  // key image (PaddedChunk on the device)
+    if (am.table) {
+      uint32_t lo = 0, hi = am.table_n;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (am.table[mid] < v) lo = mid + 1; else hi = mid;
+      }
+      if (lo < am.table_n && am.table[lo] == v) return lo;
+      atomicOr(flags, kFlagBinmap);
+      return 0;
+    }
+    return (v - am.key_lo) & am.key_mask;
+  } else if constexpr (AFFINE) {
     if (am.table) {  // ValueIndex::bin_of (value_index.hpp:40-45): exact match in the table
       const uint32_t k = float_order_key_bits(__float_as_uint(static_cast<float>(v)));
       uint32_t lo = 0, hi = am.table_n;
@@ -123,7 +137,9 @@ __global__ void __launch_bounds__(256) k_tour3(Slab s, int64_t seg, AffineMap am
   const int64_t i1 = min(i0 + seg, s.own1);
   if (j < s.w1 && i0 < i1) {  // warp-uniform (a warp is one row j)
     const bool kin = k >= 0 && k < s.w2;
-    const bool own = kin && lane >= 1 && lane <= LANES_OWNED;
+    const int64_t OW1 = s.own_j1() - s.oj0, OW2 = s.own_k1() - s.ok0;
+    const bool own = kin && lane >= 1 && lane <= LANES_OWNED && j >= s.oj0 && j < s.own_j1() &&
+                     k >= s.ok0 && k < s.own_k1();
     const bool up = j > 0, dn = j + 1 < s.w1;
     const int64_t rp = s.row_pitch(), pp = s.plane_pitch();
     const T* ctr = static_cast<const T*>(s.base) + j * rp + (kin ? k : 0) - s.plane0 * pp;
@@ -174,7 +190,7 @@ __global__ void __launch_bounds__(256) k_tour3(Slab s, int64_t seg, AffineMap am
       plane(i + 1, nxt, vnxt);
       const uint32_t X = tour::xmask(nxt, cur);
       if (own) {
-        const int64_t vox = ((i - s.own0) * s.w1 + j) * s.w2 + k;
+        const int64_t vox = ((i - s.own0) * OW1 + (j - s.oj0)) * OW2 + (k - s.ok0);
         if constexpr (HIST) {
           sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS3>(cur.I, X, Xp));
         } else if constexpr (MODE == kChanges) {
@@ -209,7 +225,8 @@ __global__ void __launch_bounds__(256) k_tour2(Slab s, int64_t seg, AffineMap am
   const int64_t i1 = min(i0 + seg, s.own1);
   if (i0 < i1) {
     const bool jin = j >= 0 && j < s.w1;
-    const bool own = jin && lane >= 1 && lane <= LANES_OWNED;
+    const int64_t OW1 = s.own_j1() - s.oj0;
+    const bool own = jin && lane >= 1 && lane <= LANES_OWNED && j >= s.oj0 && j < s.own_j1();
     const int64_t pp = s.plane_pitch();
     const T* ctr = static_cast<const T*>(s.base) + (jin ? j : 0) - s.plane0 * pp;
     auto row = [&](int64_t i, tour::Plane<tour::NB2>& P, T& val) {
@@ -237,7 +254,7 @@ __global__ void __launch_bounds__(256) k_tour2(Slab s, int64_t seg, AffineMap am
       row(i + 1, nxt, vnxt);
       const uint32_t X = tour::xmask(nxt, cur);
       if (own) {
-        const int64_t vox = (i - s.own0) * s.w1 + j;
+        const int64_t vox = (i - s.own0) * OW1 + (j - s.oj0);
         if constexpr (HIST) {
           sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS2>(cur.I, X, Xp));
         } else if constexpr (MODE == kChanges) {
@@ -337,6 +354,111 @@ cudaError_t launch_generic_changes(const Slab& s, int dtype, int8_t* out, int sm
 cudaError_t launch_generic_faces(const Slab& s, int dtype, uint32_t* out, int sms,
                                  cudaStream_t st) {
   return launch_generic_out<kFaces>(s, dtype, out, sms, st);
+}
+
+// ---------------------------------------------------------------- padded chunks
+// A PaddedChunk's extended storage (chunk.hpp:50-127: u8 -> int16 with the
+// sentinel 256, u16 -> int32, f32 -> float with +inf) turned into a key image
+// on the device: order-preserving uint32 keys of exactly the stored values,
+// collar included, so ties with the collar behave as in the reference.  2D
+// chunks keep only the middle column of the padded axis 2.  `interior`
+// writes only the owned voxels (rows 1..np-2, collar stripped) densely.
+__global__ void k_chunk_keys(const void* __restrict__ padded, int etype, uint64_t np, uint64_t w1p,
+                             uint64_t w2p, int is2d, int interior, uint32_t* __restrict__ keys) {
+  const uint64_t o0 = interior ? 1 : 0, o1 = interior ? 1 : 0, o2 = (interior || is2d) ? 1 : 0;
+  const uint64_t n0 = np - 2 * o0, n1 = w1p - 2 * o1, n2 = is2d ? 1 : w2p - 2 * o2;
+  const uint64_t n = n0 * n1 * n2;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < n;
+       t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = t % n2, r = (t / n2) % n1, p = t / (n1 * n2);
+    const uint64_t src = ((p + o0) * w1p + (r + o1)) * w2p + (c + o2);
+    uint32_t k;
+    if (etype == 0)
+      k = (uint32_t)((int32_t)static_cast<const int16_t*>(padded)[src] + 32768);
+    else if (etype == 1)
+      k = (uint32_t)static_cast<const int32_t*>(padded)[src] ^ 0x80000000u;
+    else
+      k = float_order_key_bits(__float_as_uint(static_cast<const float*>(padded)[src]));
+    keys[t] = k;
+  }
+}
+
+cudaError_t launch_chunk_keys(const void* padded, int etype, uint64_t np, uint64_t w1p,
+                              uint64_t w2p, bool is2d, bool interior, uint32_t* keys, int sms,
+                              cudaStream_t st) {
+  k_chunk_keys<<<sms * 4, 256, 0, st>>>(padded, etype, np, w1p, w2p, is2d ? 1 : 0,
+                                        interior ? 1 : 0, keys);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keyimage(const Slab& s, int mode, const AffineMap& am, int64_t* ghist,
+                            uint32_t nbins, uint32_t* flags, void* out, int sms, cudaStream_t st) {
+  switch (mode) {
+    case kChanges:
+      return launch_generic_t<uint32_t, true, kChanges>(s, am, nullptr, 0, nullptr, out, sms, st);
+    case kFaces:
+      return launch_generic_t<uint32_t, true, kFaces>(s, am, nullptr, 0, nullptr, out, sms, st);
+    default:
+      if (nbins <= kSmemBinLimit)
+        return launch_generic_t<uint32_t, true, kHistSmem>(s, am, ghist, nbins, flags, nullptr,
+                                                           sms, st);
+      return launch_generic_t<uint32_t, true, kHistGlobal>(s, am, ghist, nbins, flags, nullptr,
+                                                           sms, st);
+  }
+}
+
+// Value lists (ValueIndex::build, merge_local): keys of n values of a dtype
+// (u8 / u16: the value; f32: the order key, NaN flagged).
+__global__ void k_value_keys(const void* __restrict__ v, int dtype, uint64_t n,
+                             uint32_t* __restrict__ keys, uint32_t* flags) {
+  bool nan = false;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t k;
+    if (dtype == 0) {
+      k = static_cast<const uint8_t*>(v)[i];
+    } else if (dtype == 1) {
+      k = static_cast<const uint16_t*>(v)[i];
+    } else {
+      const float x = static_cast<const float*>(v)[i];
+      nan |= x != x;
+      k = float_order_key_bits(__float_as_uint(x));
+    }
+    keys[i] = k;
+  }
+  if (nan) atomicOr(flags, kFlagNaN);
+}
+
+// merge_local's incoming entries: sums[i] = local[bin of value i], bin = the
+// value (u8 / u16 keys) or the position i (a float value index).
+__global__ void k_gather_local(const uint32_t* __restrict__ keys, int by_value, uint64_t n,
+                               const int64_t* __restrict__ local, uint64_t nlocal,
+                               int64_t* __restrict__ sums, uint32_t* flags) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = by_value ? keys[i] : i;
+    if (b < nlocal) {
+      sums[i] = local[b];
+    } else {
+      sums[i] = 0;
+      atomicOr(flags, kFlagBinmap);
+    }
+  }
+}
+
+cudaError_t launch_value_keys(const void* v, int dtype, uint64_t n, uint32_t* keys,
+                              uint32_t* flags, int sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_value_keys<<<sms * 4, 256, 0, st>>>(v, dtype, n, keys, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gather_local(const uint32_t* keys, bool by_value, uint64_t n,
+                                const int64_t* local, uint64_t nlocal, int64_t* sums,
+                                uint32_t* flags, int sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  k_gather_local<<<sms * 2, 256, 0, st>>>(keys, by_value ? 1 : 0, n, local, nlocal, sums, flags);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- order keys

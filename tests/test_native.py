@@ -70,3 +70,16 @@ def test_cpp_curve_csv_matches_reference_writer(tmp_path):
         fh.write(chi.tobytes())
     mine = subprocess.run([_bin("test_api"), "csv", str(f)], capture_output=True, check=True).stdout
     assert mine == oracle.ref_csv(t, chi)
+
+
+def test_reference_tests_compile_against_the_drop_in():
+    """The reference's own test programs (proj/tests/test_streaming.cpp,
+    test_kernel.cpp, test_value_index.cpp, test_curve.cpp, acceptance.cpp)
+    compile UNMODIFIED with include/ first on the include path -- the
+    drop-in's headers provide every symbol they use.  (They run on the GPU
+    in tests/test_gpu_reference_suite.py.)"""
+    if not os.path.isdir("/root/reference/proj/tests"):
+        pytest.skip("the reference sources exist only in the build container")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    for t in ["test_streaming", "test_kernel", "test_value_index", "test_curve", "acceptance"]:
+        assert os.path.exists(os.path.join(BIN, "ref_" + t)), t
