@@ -28,6 +28,7 @@ namespace eccb {
 namespace {
 
 constexpr int NT = 1024;
+static_assert(hist16::no_wrap(NT, 1, 3), "2D changes reach -3: the packed halves could wrap");
 
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;

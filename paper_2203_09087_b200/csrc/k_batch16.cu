@@ -37,6 +37,7 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 #define ECC_HGRP 8
 #endif
 constexpr int HGRP = ECC_HGRP;  // pixels per atomic group (divides 32)
+static_assert(hist16::no_wrap(NT, HGRP, 3), "2D changes reach -3: the packed halves could wrap");
 constexpr uint32_t BIAS = 0x80008000u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

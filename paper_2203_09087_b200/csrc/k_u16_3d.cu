@@ -19,9 +19,11 @@
 //    code transpose produce signed bytes that one PRMT sign-extends.
 //  * Histogram: 65536 signed 16-bit halves packed two per word in shared
 //    memory, each biased by 32768 (hist16.cuh): an update that leaves its
-//    half outside [-8192, 8191] moves the half's current value to the global
+//    half outside [-4096, 4095] moves the half's current value to the global
 //    int64 histogram with a compare-and-swap, so the half is reset to exactly
-//    0 and never nears the 16-bit wrap.  Occupancy is a 65536-bit map.
+//    0; the group size keeps the worst-case drift before the first reset
+//    below the wrap (hist16.cuh's bound, asserted below).  Occupancy is a
+//    65536-bit map.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <algorithm>
@@ -52,9 +54,11 @@ constexpr uint32_t BIAS = 0x80008000u;  // both halves at 32768
 #define ECC_AFF_U 8
 #endif
 #ifndef ECC_U16_GRP
-#define ECC_U16_GRP 15
+#define ECC_U16_GRP 10
 #endif
 constexpr int GRP = ECC_U16_GRP;  // voxels per atomic group (divides 30)
+static_assert(30 % GRP == 0, "a group size divides the 30 owned bits");
+static_assert(hist16::no_wrap(NW * 32, GRP, 7), "3D changes reach -7: the packed halves could wrap");
 
 struct Geom {
   int W0, W1, W2, plane0, own0, P, Gy, Gz, ncols, seglen, nunits;

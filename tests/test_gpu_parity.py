@@ -416,6 +416,38 @@ def test_u16_spill_path_isolated_minima(ctx):
     assert got.changes[0] == 256 ** 3
 
 
+def _minus7_lattice(shape, a, b, c):
+    """2 x 2 x 2-periodic lattice whose class-(even, even, even) voxels all
+    have change -7 (the most negative 3D change): value `a`
+    there, `c` < a on the (odd, odd, odd) corners, `b` > a elsewhere -- each
+    such voxel wins its 6 face pairs and 12 edge quads and no cube, -1 + 6 -
+    12 + 0 = -7 -- so one bin takes -7 from an eighth of all voxels."""
+    x, y, z = np.indices(shape)
+    img = np.full(shape, b, dtype=np.uint16)
+    img[(x % 2 == 0) & (y % 2 == 0) & (z % 2 == 0)] = a
+    img[(x % 2 == 1) & (y % 2 == 1) & (z % 2 == 1)] = c
+    return img
+
+
+@pytest.mark.parametrize("shape", [(64, 96, 256), (130, 66, 300)])
+def test_hist16_adversarial_minus7_lattice(ctx, shape):
+    """The packed 16-bit histogram's worst case (hist16.cuh bound): every
+    value-`a` voxel pushes the same half down by 7, so every CTA's half
+    crosses the band again and again and the exact compare-and-swap spill
+    runs under full contention; the VCEC must equal the oracle's."""
+    img = _minus7_lattice(shape, 1000, 50000, 7)
+    got = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert _same(got.values, got.changes, v, c)
+    n_a = int(((np.indices(shape) % 2) == 0).all(axis=0).sum())
+    i = int(np.searchsorted(v, 1000))
+    assert c[i] <= -7 * n_a // 2  # the adversarial bin really is hot
+    # the same lattice as quantised f32 through the affine key pass
+    f = img.astype(np.float32) * np.float32(2.0 ** -16)
+    got = ctx.vcec(f, binmap=eb.quantised_binmap(65536))
+    assert np.array_equal(got.changes, c)
+
+
 def test_f32_sorted_2d_infinities_and_signed_zeros(ctx):
     """The reference's quirks on the sorted f32 path in 2D:
     +inf pixels tie with the +inf collar sentinel, -0 merges into +0."""
