@@ -60,23 +60,28 @@ namespace u83d {
 using u8fin::flush_and_finalize;
 
 #ifndef ECC_U83D_NW
-#define ECC_U83D_NW 4
+#define ECC_U83D_NW 8
 #endif
 constexpr int NW = ECC_U83D_NW;  // warps per CTA
 #ifndef ECC_U83D_NS
-#define ECC_U83D_NS 4
+#define ECC_U83D_NS 2
 #endif
 constexpr int NS = ECC_U83D_NS;  // TMA ring stages per warp (a power of two)
+#ifndef ECC_U83D_PB
+#define ECC_U83D_PB 2
+#endif
+constexpr int PB = ECC_U83D_PB;  // planes per TMA box (1 or 2): one wait + one refill per box
 constexpr int BOXZ = 48;   // box bytes along axis 2 (window of 32 + alignment)
 constexpr int BOXY = 32;   // rows per box (one per lane)
-constexpr int STAGE = BOXZ * BOXY;
+constexpr int PLANE_BYTES = BOXZ * BOXY;
+constexpr int STAGE = PLANE_BYTES * PB;
 constexpr int NCODE = 16;
 constexpr int HIST_WORDS = NCODE * 256;
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + HIST_WORDS * 4;
 #ifndef ECC_U83D_CTAS
-#define ECC_U83D_CTAS 4
+#define ECC_U83D_CTAS 2
 #endif
 constexpr int CTAS_PER_SM = ECC_U83D_CTAS;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -137,7 +142,8 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
 
 // Position of one warp in its sequence of work units (unit u = gw + i *
 // nwt, segment-major) and of the plane step k in [0, len + 2) within it
-// (one halo plane on each side along axis 0).
+// (one halo plane on each side along axis 0); the producer moves a box of
+// PB planes at a time.
 struct Cursor {
   int u, k, len, x0, ys, ye, zs, ze;
   __device__ __forceinline__ void set(const Geom& g) {
@@ -157,7 +163,8 @@ struct Cursor {
   }
   __device__ __forceinline__ bool valid(const Geom& g) const { return u < g.nunits; }
   __device__ __forceinline__ void next(const Geom& g, int nwt) {
-    if (++k == len + 2) {
+    k += PB;
+    if (k >= len + 2) {
       u += nwt;
       k = 0;
       if (u < g.nunits) set(g);
@@ -221,17 +228,19 @@ struct Codes {
 // X-1.  KIND 0: the unit's first (halo) plane, tournament only; KIND 1: +
 // x comparisons against P (P may be the x = -1 collar); KIND 2: + the
 // changes of P (X-1 is an owned plane).
-template <bool CH, int KIND, class Issue>
+template <bool CH, int KIND, int SUB, bool RELEASE, class Issue>
 __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int zs,
                                            const RunGeom& rg, uint32_t& step,
                                            uint8_t (*myring)[STAGE], uint64_t* myfull,
                                            const uint32_t hist_s, const Cursor& pc, int lane,
                                            Row& P, Row& N, XCarry& xc, Issue& issue) {
+  // `step` counts boxes: plane SUB of the box in ring slot step % NS
   const uint32_t slot = step & (NS - 1);
   const uint32_t phase = (step / NS) & 1u;
-  mbar_wait(&myfull[slot], phase);
+  if (SUB == 0) mbar_wait(&myfull[slot], phase);
   {
-    const uint4* rowp = reinterpret_cast<const uint4*>(myring[slot] + lane * BOXZ);
+    const uint4* rowp =
+        reinterpret_cast<const uint4*>(myring[slot] + SUB * PLANE_BYTES + lane * BOXZ);
     const uint4 q0 = rowp[0], q1 = rowp[1], q2 = rowp[2];
     const uint32_t Wd[12] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
                              q2.x, q2.y, q2.z, q2.w};
@@ -248,10 +257,13 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
 #undef ECC_WINDOW
   }
   __syncwarp();
-  // refill this slot with the load NS steps ahead.  Every lane has consumed
-  // its LDS results (the funnel shifts above) before the __syncwarp, so the
-  // async-proxy write cannot overtake a generic read of the slot.
-  if (pc.valid(g)) issue(slot);
+  // after the box's last plane: refill this slot with the box NS ahead.
+  // Every lane has consumed its LDS results (the funnel shifts above) before
+  // the __syncwarp, so the async-proxy write cannot overtake a generic read.
+  if (RELEASE) {
+    if (pc.valid(g)) issue(slot);
+    ++step;
+  }
   uint32_t (&C)[8] = N.C;
   bits::byte_interleave(N.W, C);
   bits::transpose8(C);
@@ -360,7 +372,6 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
     xc.gxa = gxa; xc.gxz = gxz; xc.gxz1 = gxz1; xc.gxy = gxy; xc.gxyu = gxyu;
     xc.g8 = g8; xc.g81 = g81; xc.g8u = g8u; xc.g8u1 = g8u1;
   }
-  ++step;
 }
 
 template <bool CH>
@@ -409,16 +420,20 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
     cc.start(g, u);
     rg.set(g, cc, lane);
     const int x0 = cc.x0, zs = cc.zs, len = cc.len;
-    sweep_step<CH, 0>(g, x0 - 1, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
-    sweep_step<CH, 1>(g, x0, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
+    // unit planes k = 0 .. len+1 (X = x0-1+k); box b holds planes 2b, 2b+1
+    // when PB == 2, one plane per box when PB == 1
+    constexpr int S1 = PB == 2 ? 1 : 0;
+    constexpr bool R0 = PB == 1;
+    sweep_step<CH, 0, 0, R0>(g, x0 - 1, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
+    sweep_step<CH, 1, S1, true>(g, x0, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
     // planes x0+1 .. x0+len: the changes of x0 .. x0+len-1
     int X = x0 + 1;
     for (; X + 1 <= x0 + len; X += 2) {
-      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
-      sweep_step<CH, 2>(g, X + 1, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
+      sweep_step<CH, 2, 0, R0>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
+      sweep_step<CH, 2, S1, true>(g, X + 1, zs, rg, step, myring, myfull, hist_s, pc, lane, A, B, xc, issue);
     }
-    if (X <= x0 + len)
-      sweep_step<CH, 2>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
+    if (X <= x0 + len)  // odd plane count: the last box's second plane is unused
+      sweep_step<CH, 2, 0, true>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
   }
   if constexpr (!CH) flush_and_finalize<NW * 32, Codes>(hist, ghist, fin);
 }
@@ -465,7 +480,7 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
     if (!enc) return cudaErrorNotSupported;
     const cuuint64_t dims[3] = {(cuuint64_t)s.w2, (cuuint64_t)s.w1, (cuuint64_t)s.nplanes};
     const cuuint64_t strides[2] = {(cuuint64_t)s.row_pitch(), (cuuint64_t)(s.w1 * s.row_pitch())};
-    const cuuint32_t box[3] = {BOXZ, BOXY, 1};
+    const cuuint32_t box[3] = {BOXZ, BOXY, PB};
     const cuuint32_t es[3] = {1, 1, 1};
     CUresult r = enc(&cache.map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(s.base), dims,
                      strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
