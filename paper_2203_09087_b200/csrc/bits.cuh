@@ -204,5 +204,35 @@ __host__ __device__ __forceinline__ void sum_code(const uint32_t (&w1)[17], cons
   out[3] = k0 ^ k1 ^ k2 ^ k3;
 }
 
+// Bit-sliced S mod 16 for S = sum_b (2 h[b] + l[b]) over the nine in-plane
+// blocks of a voxel (h[b] & l[b] == 0, so each block adds 0, 1 or 2): the
+// per-block form of the tournament sum, change + 9 = sum_b q_b with
+// q_b = 1 + s_b I_b (X_b - Xp_b) (k_u8_3d.cu).  12 full adders, one half
+// adder and one 3-input XOR; out[k] bit p = bit k of S at lane-bit p.
+__host__ __device__ __forceinline__ void sum_blocks9(const uint32_t (&h)[9], const uint32_t (&l)[9],
+                                                     uint32_t (&out)[4]) {
+  // weight 1: the nine l's
+  uint32_t a0, c0, a1, c1, a2, c2, c3;
+  fa3(l[0], l[1], l[2], a0, c0);
+  fa3(l[3], l[4], l[5], a1, c1);
+  fa3(l[6], l[7], l[8], a2, c2);
+  fa3(a0, a1, a2, out[0], c3);
+  // weight 2: the nine h's and four carries
+  uint32_t b0, d0, b1, d1, b2, d2, b3, d3, e0, f0, f1;
+  fa3(h[0], h[1], h[2], b0, d0);
+  fa3(h[3], h[4], h[5], b1, d1);
+  fa3(h[6], h[7], h[8], b2, d2);
+  fa3(c0, c1, c2, b3, d3);
+  fa3(b0, b1, b2, e0, f0);
+  fa3(e0, b3, c3, out[1], f1);
+  // weight 4: six carries
+  uint32_t g0, k0, g1, k1;
+  fa3(d0, d1, d2, g0, k0);
+  fa3(d3, f0, f1, g1, k1);
+  out[2] = g0 ^ g1;
+  // weight 8 (mod 16): three carries
+  out[3] = k0 ^ k1 ^ (g0 & g1);
+}
+
 }  // namespace bits
 }  // namespace eccb

@@ -26,18 +26,20 @@
 // change is  -1 + #2-blocks won - #4-blocks won + #8-blocks won.  Block
 // winners come from a tournament: 7 bit-sliced comparisons (z, y, yz in the
 // plane; x, xz, xy, xyz against the next plane) and 3 bit-sliced minimum
-// selections per voxel.  The x-side blocks pair up (the block towards x+1
-// and the block towards x-1 share their in-plane factor), so each pair is
-// entered into the sum as a 2-bit number built by two LOP3s; 17 weight-1
-// and 9 weight-2 bit vectors then go through a 19-full-adder carry-save
-// tree (bits::sum_code), giving code = (change + 17) mod 16 per voxel.
+// selections per voxel.  Each of the voxel's nine in-plane blocks b (the
+// voxel, 4 pairs, 4 yz 4-blocks) contributes s_b I_b (X_b - Xp_b) -- I_b:
+// the voxel wins b in its plane; X_b / Xp_b: the next / this plane's copy of
+// b wins the axis-0 comparison (tourney.cuh derives it) -- entered as
+// q_b = 1 + that in {0, 1, 2} = 2 h_b + l_b with two LOP3s; the 18 bit
+// vectors go through a 12-full-adder carry-save tree (bits::sum_blocks9)
+// giving code = change + 9 in [2, 14] per voxel.
 //
 // Histogram (K2).  The 4 code planes are transposed back to bytes and each
 // voxel does ONE shared-memory atomic increment at hist[code][value] (one
 // PRMT builds the index from the value byte and the code byte); the table
 // (16 x 256 x u32 per CTA) is reduced to per-value change sums and counts
 // once at the end and flushed with int64 global atomics.  Voxels the lane
-// does not own go to code 8, which no real change produces.
+// does not own go to code 15, which no real change produces.
 //
 // Collar.  Voxels outside the image hold 255 in the planes; that is only
 // wrong when an outside voxel is the EARLIER side of a comparison (the
@@ -213,14 +215,12 @@ struct RunGeom {
   }
 };
 
-__device__ __forceinline__ int decode_change(uint32_t code) {
-  return code >= 10 ? (int)code - 17 : (int)code - 1;
-}
+__device__ __forceinline__ int decode_change(uint32_t code) { return (int)code - 9; }
 
-// code = (change + 17) mod 16; 8 = not emitted
+// code = change + 9 in [2, 14]; 15 = not emitted
 struct Codes {
   static constexpr int n = NCODE;
-  static __device__ __forceinline__ bool live(int c) { return c != 8; }
+  static __device__ __forceinline__ bool live(int c) { return c != 15; }
   static __device__ __forceinline__ int change(int c) { return decode_change((uint32_t)c); }
 };
 
@@ -313,32 +313,39 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
       // ---- changes of row X-1: each voxel gathers its 26 block wins
       const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
       const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
-      const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;  // wins its z+ / z- pair
-      const uint32_t Yf0 = ~P.gy, Yf1 = gyu;      // wins its y+ / y- pair
-      const uint32_t I00 = Z0 & ~P.gyz;           // wins the four yz 4-blocks
-      const uint32_t I01 = (P.gz & ~P.gyz) << 1;
-      const uint32_t I10 = Z0 & gyzu;
-      const uint32_t I11 = (P.gz & gyzu) << 1;
-      // x-side pairs F * (a + b): sum bit F & (a ^ b), carry bit F & a & b;
-      // the 4 edge pairs enter negated (-e = ~e - 1).
-      uint32_t w1[17], w2[9];
-      w1[0] = Z0; w1[1] = Z1; w1[2] = Yf0; w1[3] = Yf1;
-      w1[4] = ~I00; w1[5] = ~I01; w1[6] = ~I10; w1[7] = ~I11;
-      w1[8] = ~(gxa ^ xc.gxa);          w2[0] = ~gxa & xc.gxa;              // x faces
-      w1[9] = ~(Z0 & ~(gxz ^ xc.gxz));  w2[1] = ~(Z0 & ~gxz & xc.gxz);      // xz edges
-      w1[10] = ~(Z1 & ~(gxz1 ^ xc.gxz1)); w2[2] = ~(Z1 & ~gxz1 & xc.gxz1);
-      w1[11] = ~(Yf0 & ~(gxy ^ xc.gxy)); w2[3] = ~(Yf0 & ~gxy & xc.gxy);   // xy edges
-      w1[12] = ~(Yf1 & ~(gxyu ^ xc.gxyu)); w2[4] = ~(Yf1 & ~gxyu & xc.gxyu);
-      w1[13] = I00 & ~(g8 ^ xc.g8);     w2[5] = I00 & ~g8 & xc.g8;          // vertices
-      w1[14] = I01 & ~(g81 ^ xc.g81);   w2[6] = I01 & ~g81 & xc.g81;
-      w1[15] = I10 & ~(g8u ^ xc.g8u);   w2[7] = I10 & ~g8u & xc.g8u;
-      w1[16] = I11 & ~(g8u1 ^ xc.g8u1); w2[8] = I11 & ~g8u1 & xc.g8u1;
-      // S = change + 17 in [10, 22]; code = S mod 16; non-emitted -> 8
+      // the nine in-plane blocks b of each voxel and I_b = "wins b inside
+      // the plane": 0 the voxel, 1 / 2 its z- / z+ pair, 3 / 4 its y- / y+
+      // pair, 5..8 the yz 4-blocks (y-,z-) (y-,z+) (y+,z-) (y+,z+)
+      const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;
+      const uint32_t I[9] = {FULL,
+                             Z1,
+                             Z0,
+                             gyu,
+                             ~P.gy,
+                             (P.gz & gyzu) << 1,
+                             Z0 & gyzu,
+                             (P.gz & ~P.gyz) << 1,
+                             Z0 & ~P.gyz};
+      // X_b: the next plane's copy of b beats this plane's; Xp_b the same
+      // one step earlier (the previous plane against this one)
+      const uint32_t X[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
+      const uint32_t Xp[9] = {xc.gxa, xc.gxz1, xc.gxz, xc.gxyu, xc.gxy,
+                              xc.g8u1, xc.g8u, xc.g81, xc.g8};
+      // q_b = 1 + s_b I_b (X_b - Xp_b) in {0, 1, 2} as 2 h_b + l_b (signs:
+      // pairs +1, the voxel and the 4-blocks -1); change + 9 = sum_b q_b
+      uint32_t h[9], l[9];
+#pragma unroll
+      for (int b = 0; b < 9; ++b) {
+        l[b] = bits::lop3<0x9F>(I[b], X[b], Xp[b]);  // ~(I & (X ^ Xp))
+        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], X[b], Xp[b])   // I & X & ~Xp
+                                  : bits::lop3<0x20>(I[b], X[b], Xp[b]);  // I & ~X & Xp
+      }
+      // S = change + 9 in [2, 14]; code = S mod 16; not emitted -> 15
       uint32_t s[4];
-      bits::sum_code(w1, w2, s);
+      bits::sum_blocks9(h, l, s);
       const uint32_t vm = rg.vm;
       uint32_t V[8];
-      bits::transpose_codes(s[0] & vm, s[1] & vm, s[2] & vm, s[3] | ~vm, V);
+      bits::transpose_codes(s[0] | ~vm, s[1] | ~vm, s[2] | ~vm, s[3] | ~vm, V);
       if constexpr (CH) {
 #pragma unroll
         for (int p = 1; p <= 30; ++p) {

@@ -54,3 +54,33 @@ int test_transpose_codes() {
   return 0;
 }
 static int run_extra = [] { return test_transpose_codes(); }();
+// (appended) sum_blocks9: every one of the 3^9 per-block (h, l) patterns
+int test_sum_blocks9() {
+  int pat = 0;
+  uint32_t h[9] = {}, l[9] = {};
+  int total = 1;
+  for (int b = 0; b < 9; ++b) total *= 3;
+  for (int base = 0; base < total; base += 32) {
+    for (int b = 0; b < 9; ++b) h[b] = l[b] = 0;
+    for (int p = 0; p < 32 && base + p < total; ++p) {
+      int t = base + p;
+      for (int b = 0; b < 9; ++b, t /= 3) {
+        const int q = t % 3;
+        if (q == 2) h[b] |= 1u << p;
+        if (q == 1) l[b] |= 1u << p;
+      }
+    }
+    uint32_t out[4];
+    eccb::bits::sum_blocks9(h, l, out);
+    for (int p = 0; p < 32 && base + p < total; ++p, ++pat) {
+      int s = 0;
+      for (int b = 0; b < 9; ++b) s += 2 * ((h[b] >> p) & 1) + ((l[b] >> p) & 1);
+      int got = 0;
+      for (int k = 0; k < 4; ++k) got |= ((out[k] >> p) & 1) << k;
+      if (got != (s & 15)) { std::printf("sum_blocks9 mismatch\n"); return 1; }
+    }
+  }
+  std::printf("sum_blocks9 ok (%d patterns)\n", pat);
+  return 0;
+}
+static int run_extra9 = [] { return test_sum_blocks9(); }();
