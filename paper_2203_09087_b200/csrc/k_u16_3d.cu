@@ -14,9 +14,10 @@
 //    the previous plane are carried (19 registers); its block minima are
 //    recomputed at the x comparison instead of stored, which keeps the
 //    16-plane state inside the register budget of 12 warps per SM.
-//  * The carry-save tree is offset by -1 so its 4 output planes ARE the
-//    change in 4-bit two's complement; replicating the sign plane makes the
-//    code transpose produce signed bytes that one PRMT sign-extends.
+//  * The per-block carry-save sum (bits::sum_blocks9, as k_u8_3d.cu) gives
+//    change + 9; adding 7 mod 16 makes its 4 planes the change in 4-bit two's
+//    complement, and replicating the sign plane makes the code transpose
+//    produce signed bytes that one PRMT sign-extends.
 //  * Histogram: 65536 signed 16-bit halves packed two per word in shared
 //    memory, each biased by 32768 (hist16.cuh): an update that leaves its
 //    half outside [-4096, 4095] moves the half's current value to the global
@@ -269,31 +270,28 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
     if constexpr (KIND == 2) {
       const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
       const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
+      // the nine in-plane blocks of each voxel (k_u8_3d.cu): I_b wins b in
+      // the plane, X_b / Xp_b the axis-0 comparisons of b, q_b = 2 h_b + l_b
       const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;
-      const uint32_t Yf0 = ~P.gy, Yf1 = gyu;
-      const uint32_t I00 = Z0 & ~P.gyz;
-      const uint32_t I01 = (P.gz & ~P.gyz) << 1;
-      const uint32_t I10 = Z0 & gyzu;
-      const uint32_t I11 = (P.gz & gyzu) << 1;
-      uint32_t w1[17], w2[9];
-      w1[0] = Z0; w1[1] = Z1; w1[2] = Yf0; w1[3] = Yf1;
-      w1[4] = ~I00; w1[5] = ~I01; w1[6] = ~I10; w1[7] = ~I11;
-      w1[8] = ~(gxa ^ xc.gxa);          w2[0] = ~gxa & xc.gxa;
-      w1[9] = ~(Z0 & ~(gxz ^ xc.gxz));  w2[1] = ~(Z0 & ~gxz & xc.gxz);
-      w1[10] = ~(Z1 & ~(gxz1 ^ xc.gxz1)); w2[2] = ~(Z1 & ~gxz1 & xc.gxz1);
-      w1[11] = ~(Yf0 & ~(gxy ^ xc.gxy)); w2[3] = ~(Yf0 & ~gxy & xc.gxy);
-      w1[12] = ~(Yf1 & ~(gxyu ^ xc.gxyu)); w2[4] = ~(Yf1 & ~gxyu & xc.gxyu);
-      w1[13] = I00 & ~(g8 ^ xc.g8);     w2[5] = I00 & ~g8 & xc.g8;
-      w1[14] = I01 & ~(g81 ^ xc.g81);   w2[6] = I01 & ~g81 & xc.g81;
-      w1[15] = I10 & ~(g8u ^ xc.g8u);   w2[7] = I10 & ~g8u & xc.g8u;
-      w1[16] = I11 & ~(g8u1 ^ xc.g8u1); w2[8] = I11 & ~g8u1 & xc.g8u1;
-      // S = change + 17; S - 1 mod 16 = change in 4-bit two's complement
+      const uint32_t I[9] = {FULL, Z1, Z0, gyu, ~P.gy, (P.gz & gyzu) << 1, Z0 & gyzu,
+                             (P.gz & ~P.gyz) << 1, Z0 & ~P.gyz};
+      const uint32_t X[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
+      const uint32_t Xp[9] = {xc.gxa, xc.gxz1, xc.gxz, xc.gxyu, xc.gxy,
+                              xc.g8u1, xc.g8u, xc.g81, xc.g8};
+      uint32_t h[9], l[9];
+#pragma unroll
+      for (int b = 0; b < 9; ++b) {
+        l[b] = bits::lop3<0x9F>(I[b], X[b], Xp[b]);  // ~(I & (X ^ Xp))
+        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], X[b], Xp[b])   // I & X & ~Xp
+                                  : bits::lop3<0x20>(I[b], X[b], Xp[b]);  // I & ~X & Xp
+      }
+      // S = change + 9; change = S + 7 mod 16 in 4-bit two's complement
       uint32_t s[4];
-      bits::sum_code(w1, w2, s);
+      bits::sum_blocks9(h, l, s);
       const uint32_t vm = rg.vm;
-      const uint32_t b1 = ~s[0], b2 = b1 & ~s[1], b3 = b2 & ~s[2];
-      const uint32_t d0 = ~s[0] & vm, d1 = (s[1] ^ b1) & vm, d2 = (s[2] ^ b2) & vm,
-                     d3 = (s[3] ^ b3) & vm;  // non-emitted voxels: change 0
+      const uint32_t c2 = s[1] | s[0], c3 = s[2] | c2;
+      const uint32_t d0 = ~s[0] & vm, d1 = ~(s[1] ^ s[0]) & vm, d2 = ~(s[2] ^ c2) & vm,
+                     d3 = (s[3] ^ c3) & vm;  // non-emitted voxels: change 0
       uint32_t V[8] = {d0, d1, d2, d3, d3, d3, d3, d3};
       bits::transpose8(V);  // byte b of V[r] = int8 change of voxel 8b + r
       const uint32_t hbase = smem_u32(hwords), pbase = smem_u32(pres);
