@@ -64,6 +64,11 @@ struct Geom {
   uint32_t four;        // = 4, opaque to ptxas (IMAD address, not an ALU LEA)
 };
 
+#ifndef ECC_U82D_MINBAND
+#define ECC_U82D_MINBAND 1
+#endif
+constexpr int MINBAND = ECC_U82D_MINBAND;  // shortest band of rows a warp sweeps
+
 struct Codes {
   static constexpr int n = 5;  // S = change + 3 in [0, 4]
   static __device__ __forceinline__ bool live(int) { return true; }
@@ -238,11 +243,12 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   g.four = 4;
   const long long cap_warps = (long long)sms * CTAS_PER_SM * NW;
   // bands of >= 32 rows (2 halo rows per band); ~4 units per resident warp
-  // when the image is large enough, else one wave of shorter bands (>= 8)
+  // when the image is large enough, else one wave of shorter bands (>= MINBAND:
+  // small images are latency-bound, so more, shorter bands finish sooner)
   long long nb = std::max<long long>(1, (4 * cap_warps) / g.nstrips);
   long long band = std::max<long long>(32, (g.P + nb - 1) / nb);
   if ((long long)((g.P + band - 1) / band) * g.nstrips < cap_warps)
-    band = std::max<long long>(8, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
+    band = std::max<long long>(MINBAND, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
   band = std::max<long long>(1, std::min<long long>(band, std::max(1, g.P)));
   g.band = (int)band;
   const long long units = (g.P + band - 1) / band * g.nstrips;
