@@ -491,6 +491,9 @@ struct ToI64 {
 
 // order-key spans up to this many values take the dense histogram (no sort)
 constexpr uint64_t kDenseKeySpan = 1ull << 24;
+// a dense table fed by at most this many voxels uses the packed one-atomic
+// words (count << 32 | sum(change + 8) stays exact: 13 * 2^28 < 2^32)
+constexpr uint64_t kPackedMaxVoxels = 1ull << 28;
 
 int merge_runs(ecc_ctx* ctx, cudaStream_t st, uint64_t n, uint64_t* m_out);
 
@@ -559,14 +562,17 @@ int sorted_slab(ecc_ctx* ctx, const Slab& s, cudaStream_t st, uint64_t* n_acc) {
     AffineMap am{};
     am.keyed = 1;
     am.key_lo = range[0];
-    CKI(ctx->hist.ensure(2 * (uint64_t)nbins * 8));
+    am.packed = n64 <= kPackedMaxVoxels;
+    const uint64_t hbytes = (am.packed ? 1 : 2) * (uint64_t)nbins * 8;
+    CKI(ctx->hist.ensure(hbytes));
     CKI(ctx->sums.ensure((uint64_t)nbins * 8));
     CKI(ctx->finscr.ensure(16ull * (nbins / 1024 + 1)));
-    CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * (uint64_t)nbins * 8, st));
+    CKR(cudaMemsetAsync(ctx->hist.p, 0, hbytes, st));
     CKR(launch_generic_accumulate(s, ECC_F32, true, am, ctx->hist.as<int64_t>(), nbins,
                                   ctx->flags.as<uint32_t>(), ctx->sms, st));
     CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, out_keys, out_sums,
-                        ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(), ctx->finscr.p, st));
+                        ctx->sums.as<int64_t>(), ctx->count.as<uint64_t>(), ctx->finscr.p, st,
+                        am.packed != 0));
     ctx->launches += 2;
     uint64_t m = 0;
     CKR(cudaMemcpyAsync(&m, ctx->count.p, 8, cudaMemcpyDeviceToHost, st));
@@ -703,18 +709,22 @@ void write_values(ecc_dtype dtype, bool sorted, const AffineMap& am, const BinRe
 // change) list (value_index.hpp:159-197).  *used = false when the span is
 // too wide (the sort path runs instead).  The curve is left in the result
 // block (layout L); keys are bins + *key_lo.
+// range_ready: flags words 1, 2 already hold the volume's order-key range
+// (fused into the smoothing pass that wrote it, ecc_bench_run).
 int dense_sorted(ecc_ctx* ctx, const Slab& s, cudaStream_t st, ResultLayout* L, uint32_t* key_lo,
-                 bool* used) {
+                 bool* used, bool range_ready = false) {
   *used = false;
   const uint64_t n64 = (uint64_t)(s.own1 - s.own0) * s.w1 * s.w2;
   if (n64 < (1ull << 20)) return ECC_OK;  // small volumes: the sort is cheap
   const float* owned = static_cast<const float*>(s.base) + (s.own0 - s.plane0) * s.w1 * s.w2;
   CKI(ctx->flags.ensure(16));
   uint32_t* mm = ctx->flags.as<uint32_t>() + 1;
-  const uint32_t init[2] = {0xFFFFFFFFu, 0u};
-  CKR(cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, st));
-  CKR(launch_key_range(owned, n64, ctx->flags.as<uint32_t>(), mm, ctx->sms, st));
-  ctx->launches += 1;
+  if (!range_ready) {
+    const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    CKR(cudaMemcpyAsync(mm, init, 8, cudaMemcpyHostToDevice, st));
+    CKR(launch_key_range(owned, n64, ctx->flags.as<uint32_t>(), mm, ctx->sms, st));
+    ctx->launches += 1;
+  }
   uint32_t range[2] = {0, 0};
   CKR(cudaMemcpyAsync(range, mm, 8, cudaMemcpyDeviceToHost, st));
   CKR(cudaStreamSynchronize(st));
@@ -724,9 +734,11 @@ int dense_sorted(ecc_ctx* ctx, const Slab& s, cudaStream_t st, ResultLayout* L, 
   AffineMap am{};
   am.keyed = 1;
   am.key_lo = range[0];
+  am.packed = n64 <= kPackedMaxVoxels;  // one 64-bit atomic per voxel (HistSink)
   const uint32_t nbins = (uint32_t)span;
-  CKI(ctx->hist.ensure(2 * (uint64_t)nbins * 8));
-  CKR(cudaMemsetAsync(ctx->hist.p, 0, 2 * (uint64_t)nbins * 8, st));
+  const uint64_t hbytes = (am.packed ? 1 : 2) * (uint64_t)nbins * 8;
+  CKI(ctx->hist.ensure(hbytes));
+  CKR(cudaMemsetAsync(ctx->hist.p, 0, hbytes, st));
   CKR(launch_generic_accumulate(s, ECC_F32, true, am, ctx->hist.as<int64_t>(), nbins,
                                 ctx->flags.as<uint32_t>(), ctx->sms, st));
   ctx->launches += 1;
@@ -737,7 +749,7 @@ int dense_sorted(ecc_ctx* ctx, const Slab& s, cudaStream_t st, ResultLayout* L, 
   CKR(launch_finalize(ctx->hist.as<int64_t>(), nbins, reinterpret_cast<uint32_t*>(d + L->bins),
                       reinterpret_cast<int64_t*>(d + L->changes),
                       reinterpret_cast<int64_t*>(d + L->chi), reinterpret_cast<uint64_t*>(d),
-                      ctx->finscr.p, st));
+                      ctx->finscr.p, st, am.packed != 0));
   ctx->launches += 1;
   *key_lo = range[0];
   *used = true;
@@ -849,8 +861,11 @@ int gaussian_weights(double sigma, int width, std::vector<double>* w) {
 
 // gaussian_smooth (datagen.hpp:108-122): axes 0, 1, 2 in turn, each skipped
 // when its extent or the width is 1; in may equal out.
+// mm (optional): the last pass also reduces the result's order-key range
+// into mm[0..1] and NaN into ctx->flags; *ranged says whether it could.
 int smooth_device(ecc_ctx* ctx, const float* in, float* out, ecc_dims d, double sigma, int width,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint32_t* mm = nullptr, bool* ranged = nullptr) {
+  if (ranged) *ranged = false;
   std::vector<double> w;
   CKI(gaussian_weights(sigma, width, &w));
   const uint64_t n = d.w0 * d.w1 * d.w2;
@@ -871,8 +886,10 @@ int smooth_device(ecc_ctx* ctx, const float* in, float* out, ecc_dims d, double 
   const bool via_tmp = na == 1 && in == out;
   for (int j = 0; j < na; ++j) {
     float* dst = (j == na - 1 && !via_tmp) ? out : ctx->sm_tmp[j & 1].as<float>();
+    const bool last = j == na - 1 && !via_tmp && mm;
     CKR(launch_convolve_axis(src, dst, d.w0, d.w1, d.w2, axes[j], ctx->sm_w.as<double>(), width,
-                             st));
+                             st, last ? mm : nullptr, last ? ctx->flags.as<uint32_t>() : nullptr,
+                             last ? ranged : nullptr));
     ctx->launches += 1;
     src = dst;
   }
@@ -1712,7 +1729,7 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
   rep->voxels = n;
   CKI(ctx->input.ensure(n * 4));
   float* img = ctx->input.as<float>();
-  CKI(ctx->flags.ensure(4));
+  CKI(ctx->flags.ensure(16));
   const auto tg0 = clk::now();
   CKR(launch_uniform_noise(img, n, seed, ctx->sms, st));
   ctx->launches += 1;
@@ -1729,18 +1746,25 @@ int ecc_bench_run(ecc_ctx* ctx, ecc_dims dims, uint64_t iterations, uint64_t see
   const Slab s = make_slab(img, dims, 0, dims.w0, 0, dims.w0);
   const auto t0 = clk::now();
   for (uint64_t it = 0; it < iterations && rc == ECC_OK; ++it) {
+    // the last smoothing pass also reduces the key range the ECC's dense
+    // histogram needs (flags words 1, 2), replacing a separate pass
+    {
+      static const uint32_t init[4] = {0u, 0xFFFFFFFFu, 0u, 0u};
+      cudaMemcpyAsync(ctx->flags.p, init, 16, cudaMemcpyHostToDevice, st);
+    }
+    bool ranged = false;
     cudaEventRecord(e0, st);
-    rc = smooth_device(ctx, img, img, dims, sigma, width, st);
+    rc = smooth_device(ctx, img, img, dims, sigma, width, st, ctx->flags.as<uint32_t>() + 1,
+                       &ranged);
     if (rc != ECC_OK) break;
     cudaEventRecord(e1, st);
     // process_image + vcec_to_ecc (streaming.hpp:332-338, curve.hpp:28-35)
     // on the sorted f32 path; the curve stays in device memory
-    cudaMemsetAsync(ctx->flags.p, 0, 4, st);
     // dense key histogram when the key span allows (no sort), else the sort
     ResultLayout L(1);
     uint32_t key_lo = 0;
     bool dense = false;
-    rc = dense_sorted(ctx, s, st, &L, &key_lo, &dense);
+    rc = dense_sorted(ctx, s, st, &L, &key_lo, &dense, ranged);
     if (rc == ECC_OK && dense) {
       rc = cudaMemcpyAsync(&m, ctx->res.p, 8, cudaMemcpyDeviceToHost, st) == cudaSuccess
                ? ECC_OK

@@ -76,6 +76,8 @@ struct AffineMap {
   uint32_t table_n = 0;
   // key images without a table: bin = (key - key_lo) & key_mask
   uint32_t key_mask = 0xFFFFFFFFu;
+  // the generic kernels' histogram as packed words (HistSink, <= 2^28 voxels)
+  int packed = 0;
 };
 
 __host__ __device__ __forceinline__ float affine_value(const AffineMap& m,

@@ -88,14 +88,19 @@ cudaError_t launch_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm, int s
                            cudaStream_t st);
 // K3; `scratch` (16 bytes per 1024 bins) enables the multi-CTA version for
 // large bin counts.
+// packed: the generic kernels' one-atomic dense table (HistSink)
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
                             int64_t* changes, int64_t* chi, uint64_t* count, void* scratch,
-                            cudaStream_t st);
+                            cudaStream_t st, bool packed = false);
 cudaError_t launch_uniform_noise(float* d, uint64_t n, uint64_t seed, int sms, cudaStream_t st);
 int gaussian_max_width();
+// mm / flags (optional): the pass also reduces its outputs' order-key range
+// (mm[0] min, mm[1] max, NaN -> flags) when it is the pipelined contiguous
+// pass; *ranged says whether it did
 cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint64_t w1,
                                  uint64_t w2, int axis, const double* d_weights, int width,
-                                 cudaStream_t st);
+                                 cudaStream_t st, uint32_t* mm = nullptr,
+                                 uint32_t* flags = nullptr, bool* ranged = nullptr);
 // batched curve serialisation (k_format.cu)
 cudaError_t launch_format_sizes(const int32_t* chi, const uint32_t* pres, uint64_t count,
                                 uint32_t nbins, int json, uint64_t* sizes, cudaStream_t st);

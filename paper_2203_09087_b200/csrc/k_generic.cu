@@ -55,16 +55,23 @@ __device__ __forceinline__ uint32_t bin_of(T v, const AffineMap& am, uint32_t* f
   }
 }
 
-// Histogram sink: per-CTA shared bins (SMEM) flushed once, or straight to
-// the global int64 histogram for large bin counts.
-template <bool SMEM>
+// Histogram sink: per-CTA shared bins (SMEM) flushed once, straight to the
+// global int64 histogram for large bin counts, or (PACKED) one 64-bit
+// atomic per voxel adding 2^32 + (change + 8) to bin's word of a packed
+// table: the high word counts the voxels, the low word is sum(change + 8),
+// exact while a table takes <= 2^28 voxels (13 * 2^28 < 2^32).  Half the
+// atomics and half the table (a 2^24-bin table fits the 126 MB L2).
+template <bool SMEM, bool PACKED = false>
 struct HistSink {
   int32_t* sums;
   uint32_t* counts;
   int64_t* ghist;
   uint32_t nbins;
   __device__ __forceinline__ void add(uint32_t bin, int change) {
-    if constexpr (SMEM) {
+    if constexpr (PACKED) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[bin]),
+                (1ull << 32) | (unsigned long long)(uint32_t)(change + 8));
+    } else if constexpr (SMEM) {
       atomicAdd(&sums[bin], change);
       atomicAdd(&counts[bin], 1u);
     } else {
@@ -75,8 +82,8 @@ struct HistSink {
   }
 };
 
-template <bool SMEM>
-__device__ __forceinline__ void sink_init(HistSink<SMEM>& h, int64_t* ghist,
+template <bool SMEM, bool PK>
+__device__ __forceinline__ void sink_init(HistSink<SMEM, PK>& h, int64_t* ghist,
                                           uint32_t nbins, int32_t* sh) {
   h.ghist = ghist;
   h.nbins = nbins;
@@ -90,8 +97,8 @@ __device__ __forceinline__ void sink_init(HistSink<SMEM>& h, int64_t* ghist,
   }
 }
 
-template <bool SMEM>
-__device__ __forceinline__ void sink_flush(HistSink<SMEM>& h) {
+template <bool SMEM, bool PK>
+__device__ __forceinline__ void sink_flush(HistSink<SMEM, PK>& h) {
   if constexpr (SMEM) {
     __syncthreads();
     const int nt = blockDim.x * blockDim.y;
@@ -113,95 +120,144 @@ enum Mode : int {
   kHistSmem = 0,   // per-bin change sums + counts, shared bins flushed per CTA
   kHistGlobal = 1, // same, straight to the global int64 histogram
   kChanges = 2,    // int8 change per owned voxel (compute_changes)
-  kFaces = 3       // uint32 introduced-face mask per owned voxel (tourney.cuh faces3/faces2)
+  kFaces = 3,      // uint32 introduced-face mask per owned voxel (tourney.cuh faces3/faces2)
+  kHistPacked = 4  // packed 64-bit count / sum words, one atomic per voxel (HistSink)
 };
 
 constexpr uint32_t FULLMASK = 0xFFFFFFFFu;
 constexpr int LANES_OWNED = 30;  // lanes 1..30 of a warp own voxels
 
 // ---------------------------------------------------------------- 3D
-// block (32, BY): lane -> axis 2 (k = 30 * blockIdx.x + lane - 1), threadIdx.y
-// -> axis 1 (one row j per warp); blockIdx.z -> segment of `seg` owned planes.
+// block (32, BY): lane -> axis 2 (k = 30 * blockIdx.x + lane - 1); each warp
+// owns TWO consecutive rows j0, j0 + 1 (j0 = 2 (BY blockIdx.y + threadIdx.y)):
+// the rows j0-1 .. j0+2 it loads serve both voxels, and the axis-1 pair and
+// 2 x 2 block between them are decided once.  blockIdx.z -> segment of
+// `seg` owned planes, swept with the previous plane's minima carried.
+struct Plane2v {
+  tour::Plane<tour::NB3> v[2];  // the two voxels (rows j0, j0 + 1)
+};
+
 template <class T, bool AFFINE, int MODE>
 __global__ void __launch_bounds__(256) k_tour3(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
                                                uint32_t nbins, uint32_t* flags, void* out) {
   extern __shared__ int32_t sh[];
-  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal;
-  HistSink<MODE == kHistSmem> sink;
+  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal || MODE == kHistPacked;
+  HistSink<MODE == kHistSmem, MODE == kHistPacked> sink;
   if constexpr (HIST) sink_init(sink, ghist, nbins, sh);
   constexpr uint32_t SENT = KeyTraits<T>::kSentinel;
   const int lane = threadIdx.x;
   const int64_t k = (int64_t)blockIdx.x * LANES_OWNED + lane - 1;
-  const int64_t j = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+  const int64_t j0 = 2 * ((int64_t)blockIdx.y * blockDim.y + threadIdx.y);
   const int64_t i0 = s.own0 + (int64_t)blockIdx.z * seg;
   const int64_t i1 = min(i0 + seg, s.own1);
-  if (j < s.w1 && i0 < i1) {  // warp-uniform (a warp is one row j)
+  if (j0 < s.w1 && i0 < i1) {  // warp-uniform (a warp is one row pair)
     const bool kin = k >= 0 && k < s.w2;
     const int64_t OW1 = s.own_j1() - s.oj0, OW2 = s.own_k1() - s.ok0;
-    const bool own = kin && lane >= 1 && lane <= LANES_OWNED && j >= s.oj0 && j < s.own_j1() &&
-                     k >= s.ok0 && k < s.own_k1();
-    const bool up = j > 0, dn = j + 1 < s.w1;
+    const bool kown = kin && lane >= 1 && lane <= LANES_OWNED && k >= s.ok0 && k < s.own_k1();
+    const bool own0 = kown && j0 >= s.oj0 && j0 < s.own_j1();
+    const bool own1 = kown && j0 + 1 >= s.oj0 && j0 + 1 < s.own_j1();
+    // rows j0-1, j0, j0+1, j0+2 present?
+    const bool rm = j0 > 0, r1 = j0 + 1 < s.w1, r2 = j0 + 2 < s.w1;
     const int64_t rp = s.row_pitch(), pp = s.plane_pitch();
-    const T* ctr = static_cast<const T*>(s.base) + j * rp + (kin ? k : 0) - s.plane0 * pp;
+    const T* ctr = static_cast<const T*>(s.base) + j0 * rp + (kin ? k : 0) - s.plane0 * pp;
 
-    // block minima and in-plane wins of plane i for this lane's voxel
-    auto plane = [&](int64_t i, tour::Plane<tour::NB3>& P, T& val) {
-      uint32_t am_ = SENT, a0 = SENT, ap = SENT;
+    // block minima and in-plane wins of plane i for the two voxels
+    auto plane = [&](int64_t i, Plane2v& P, T (&val)[2]) {
+      uint32_t am_ = SENT, a0 = SENT, a1 = SENT, a2 = SENT;
       if (kin && i >= 0 && i < s.w0) {
         const T* pc = ctr + i * pp;
-        val = __ldg(pc);
-        a0 = KeyTraits<T>::key(val);
-        if (up) am_ = KeyTraits<T>::key(__ldg(pc - rp));
-        if (dn) ap = KeyTraits<T>::key(__ldg(pc + rp));
+        val[0] = __ldg(pc);
+        a0 = KeyTraits<T>::key(val[0]);
+        if (rm) am_ = KeyTraits<T>::key(__ldg(pc - rp));
+        if (r1) {
+          val[1] = __ldg(pc + rp);
+          a1 = KeyTraits<T>::key(val[1]);
+        }
+        if (r2) a2 = KeyTraits<T>::key(__ldg(pc + 2 * rp));
       }
       // the same rows at k + 1 (lane + 1)
       const uint32_t bm_ = __shfl_down_sync(FULLMASK, am_, 1);
       const uint32_t b0 = __shfl_down_sync(FULLMASK, a0, 1);
-      const uint32_t bp = __shfl_down_sync(FULLMASK, ap, 1);
-      // pairs along axis 2 anchored at k (rows j-1, j, j+1)
-      const uint32_t mzm = min(am_, bm_), mz0 = min(a0, b0), mzp = min(ap, bp);
-      const bool hz0 = b0 < a0;        // k+1 beats k in row j
-      // pairs along axis 1 anchored at (j-1, k) and (j, k)
-      const bool hym = a0 < am_, hy0 = ap < a0;
-      // 2 x 2 blocks anchored at (j-1, k), (j, k): the later row's pair wins?
-      const bool hqm = mz0 < mzm, hq0 = mzp < mz0;
-      const uint32_t mqm = min(mzm, mz0), mq0 = min(mz0, mzp);
+      const uint32_t b1 = __shfl_down_sync(FULLMASK, a1, 1);
+      const uint32_t b2 = __shfl_down_sync(FULLMASK, a2, 1);
+      // pairs along axis 2 anchored at k (rows j0-1 .. j0+2)
+      const uint32_t mzm = min(am_, bm_), mz0 = min(a0, b0), mz1 = min(a1, b1), mz2 = min(a2, b2);
+      const bool hz0 = b0 < a0, hz1 = b1 < a1;  // k+1 beats k in rows j0, j0+1
+      // pairs along axis 1 anchored at rows j0-1, j0, j0+1: the later row wins?
+      const bool hym = a0 < am_, hy0 = a1 < a0, hy1 = a2 < a1;
+      // 2 x 2 blocks anchored at rows j0-1, j0, j0+1: the later row's pair wins?
+      const bool hqm = mz0 < mzm, hq0 = mz1 < mz0, hq1 = mz2 < mz1;
+      const uint32_t mqm = min(mzm, mz0), mq0 = min(mz0, mz1), mq1 = min(mz1, mz2);
       // the blocks anchored at k - 1 come from lane - 1
       const uint32_t Lmz0 = __shfl_up_sync(FULLMASK, mz0, 1);
+      const uint32_t Lmz1 = __shfl_up_sync(FULLMASK, mz1, 1);
       const uint32_t Lmqm = __shfl_up_sync(FULLMASK, mqm, 1);
       const uint32_t Lmq0 = __shfl_up_sync(FULLMASK, mq0, 1);
-      const uint32_t Lb = __shfl_up_sync(FULLMASK, (uint32_t)hz0 | ((uint32_t)hqm << 1) |
-                                                       ((uint32_t)hq0 << 2), 1);
-      const uint32_t Lhz0 = Lb & 1u, Lhqm = (Lb >> 1) & 1u, Lhq0 = (Lb >> 2) & 1u;
-      const uint32_t nz0 = !hz0;
-      P.M[0] = a0;   P.M[1] = Lmz0; P.M[2] = mz0; P.M[3] = min(am_, a0); P.M[4] = min(a0, ap);
-      P.M[5] = Lmqm; P.M[6] = mqm;  P.M[7] = Lmq0; P.M[8] = mq0;
-      P.I = 1u | (Lhz0 << 1) | (nz0 << 2) | ((uint32_t)hym << 3) | ((uint32_t)!hy0 << 4) |
+      const uint32_t Lmq1 = __shfl_up_sync(FULLMASK, mq1, 1);
+      const uint32_t Lb = __shfl_up_sync(
+          FULLMASK, (uint32_t)hz0 | ((uint32_t)hz1 << 1) | ((uint32_t)hqm << 2) |
+                        ((uint32_t)hq0 << 3) | ((uint32_t)hq1 << 4), 1);
+      const uint32_t Lhz0 = Lb & 1u, Lhz1 = (Lb >> 1) & 1u, Lhqm = (Lb >> 2) & 1u,
+                     Lhq0 = (Lb >> 3) & 1u, Lhq1 = (Lb >> 4) & 1u;
+      const uint32_t nz0 = !hz0, nz1 = !hz1;
+      const uint32_t my_m = min(am_, a0), my_0 = min(a0, a1), my_1 = min(a1, a2);
+      tour::Plane<tour::NB3>& v = P.v[0];
+      v.M[0] = a0;   v.M[1] = Lmz0; v.M[2] = mz0; v.M[3] = my_m; v.M[4] = my_0;
+      v.M[5] = Lmqm; v.M[6] = mqm;  v.M[7] = Lmq0; v.M[8] = mq0;
+      v.I = 1u | (Lhz0 << 1) | (nz0 << 2) | ((uint32_t)hym << 3) | ((uint32_t)!hy0 << 4) |
             ((Lhz0 & Lhqm) << 5) | ((nz0 & (uint32_t)hqm) << 6) | ((Lhz0 & (Lhq0 ^ 1u)) << 7) |
             ((nz0 & (uint32_t)!hq0) << 8);
+      tour::Plane<tour::NB3>& w = P.v[1];
+      w.M[0] = a1;   w.M[1] = Lmz1; w.M[2] = mz1; w.M[3] = my_0; w.M[4] = my_1;
+      w.M[5] = Lmq0; w.M[6] = mq0;  w.M[7] = Lmq1; w.M[8] = mq1;
+      w.I = 1u | (Lhz1 << 1) | (nz1 << 2) | ((uint32_t)hy0 << 3) | ((uint32_t)!hy1 << 4) |
+            ((Lhz1 & Lhq0) << 5) | ((nz1 & (uint32_t)hq0) << 6) | ((Lhz1 & (Lhq1 ^ 1u)) << 7) |
+            ((nz1 & (uint32_t)!hq1) << 8);
     };
 
-    tour::Plane<tour::NB3> cur, nxt;
-    T vcur = T(0), vnxt = T(0);
-    plane(i0 - 1, nxt, vnxt);
-    plane(i0, cur, vcur);
-    uint32_t Xp = tour::xmask(cur, nxt);
-    for (int64_t i = i0; i < i1; ++i) {
-      plane(i + 1, nxt, vnxt);
-      const uint32_t X = tour::xmask(nxt, cur);
-      if (own) {
-        const int64_t vox = ((i - s.own0) * OW1 + (j - s.oj0)) * OW2 + (k - s.ok0);
-        if constexpr (HIST) {
-          sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS3>(cur.I, X, Xp));
-        } else if constexpr (MODE == kChanges) {
-          static_cast<int8_t*>(out)[vox] = (int8_t)tour::change_of<tour::POS3>(cur.I, X, Xp);
-        } else {
-          static_cast<uint32_t*>(out)[vox] = tour::faces3(cur.I, X, Xp);
+    auto emit = [&](int64_t i, const Plane2v& C, const uint32_t (&X)[2], const uint32_t (&Xp)[2],
+                    const T (&val)[2]) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (r == 0 ? own0 : own1) {
+          const int64_t vox = ((i - s.own0) * OW1 + (j0 + r - s.oj0)) * OW2 + (k - s.ok0);
+          if constexpr (HIST) {
+            const uint32_t bin = (AFFINE && am.keyed && !am.table)
+                                     ? C.v[r].M[0] - am.key_lo
+                                     : bin_of<T, AFFINE>(val[r], am, flags);
+            sink.add(bin, tour::change_of<tour::POS3>(C.v[r].I, X[r], Xp[r]));
+          } else if constexpr (MODE == kChanges) {
+            static_cast<int8_t*>(out)[vox] = (int8_t)tour::change_of<tour::POS3>(C.v[r].I, X[r], Xp[r]);
+          } else {
+            static_cast<uint32_t*>(out)[vox] = tour::faces3(C.v[r].I, X[r], Xp[r]);
+          }
         }
       }
-      Xp = X;
-      cur = nxt;
-      vcur = vnxt;
+    };
+    auto xm = [&](const Plane2v& N, const Plane2v& C, uint32_t (&X)[2]) {
+      X[0] = tour::xmask(N.v[0], C.v[0]);
+      X[1] = tour::xmask(N.v[1], C.v[1]);
+    };
+
+    // two planes per iteration with the roles of A and B swapped: no copies
+    Plane2v A, B;
+    T va[2] = {T(0), T(0)}, vb[2] = {T(0), T(0)};
+    uint32_t X[2], Xp[2];
+    plane(i0 - 1, A, va);
+    plane(i0, B, vb);
+    xm(B, A, Xp);
+    for (int64_t i = i0; i < i1; i += 2) {
+      plane(i + 1, A, va);  // plane i lives in B
+      xm(A, B, X);
+      emit(i, B, X, Xp, vb);
+      Xp[0] = X[0];
+      Xp[1] = X[1];
+      if (i + 1 >= i1) break;
+      plane(i + 2, B, vb);  // plane i + 1 lives in A
+      xm(B, A, X);
+      emit(i + 1, A, X, Xp, va);
+      Xp[0] = X[0];
+      Xp[1] = X[1];
     }
   }
   if constexpr (HIST) sink_flush(sink);
@@ -214,8 +270,8 @@ template <class T, bool AFFINE, int MODE>
 __global__ void __launch_bounds__(256) k_tour2(Slab s, int64_t seg, AffineMap am, int64_t* ghist,
                                                uint32_t nbins, uint32_t* flags, void* out) {
   extern __shared__ int32_t sh[];
-  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal;
-  HistSink<MODE == kHistSmem> sink;
+  constexpr bool HIST = MODE == kHistSmem || MODE == kHistGlobal || MODE == kHistPacked;
+  HistSink<MODE == kHistSmem, MODE == kHistPacked> sink;
   if constexpr (HIST) sink_init(sink, ghist, nbins, sh);
   constexpr uint32_t SENT = KeyTraits<T>::kSentinel;
   const int lane = threadIdx.x & 31;
@@ -256,7 +312,9 @@ __global__ void __launch_bounds__(256) k_tour2(Slab s, int64_t seg, AffineMap am
       if (own) {
         const int64_t vox = (i - s.own0) * OW1 + (j - s.oj0);
         if constexpr (HIST) {
-          sink.add(bin_of<T, AFFINE>(vcur, am, flags), tour::change_of<tour::POS2>(cur.I, X, Xp));
+          const uint32_t bin = (AFFINE && am.keyed && !am.table) ? cur.M[0] - am.key_lo
+                                                                 : bin_of<T, AFFINE>(vcur, am, flags);
+          sink.add(bin, tour::change_of<tour::POS2>(cur.I, X, Xp));
         } else if constexpr (MODE == kChanges) {
           static_cast<int8_t*>(out)[vox] = (int8_t)tour::change_of<tour::POS2>(cur.I, X, Xp);
         } else {
@@ -285,7 +343,7 @@ cudaError_t launch_generic_t(const Slab& s, const AffineMap& am, int64_t* ghist,
   dim3 block, grid;
   if (d3) {
     block = dim3(32, 8, 1);
-    grid = dim3((unsigned)((s.w2 + LANES_OWNED - 1) / LANES_OWNED), (unsigned)((s.w1 + 7) / 8), 1);
+    grid = dim3((unsigned)((s.w2 + LANES_OWNED - 1) / LANES_OWNED), (unsigned)((s.w1 + 15) / 16), 1);
   } else {
     block = dim3(256, 1, 1);
     grid = dim3((unsigned)((s.w1 + 8 * LANES_OWNED - 1) / (8 * LANES_OWNED)), 1, 1);
@@ -309,6 +367,8 @@ template <class T, bool AFFINE>
 cudaError_t launch_generic_hist(const Slab& s, const AffineMap& am, int64_t* ghist,
                                 uint32_t nbins, uint32_t* flags, int sms,
                                 cudaStream_t st) {
+  if (am.packed)
+    return launch_generic_t<T, AFFINE, kHistPacked>(s, am, ghist, nbins, flags, nullptr, sms, st);
   if (nbins <= kSmemBinLimit)
     return launch_generic_t<T, AFFINE, kHistSmem>(s, am, ghist, nbins, flags, nullptr, sms, st);
   return launch_generic_t<T, AFFINE, kHistGlobal>(s, am, ghist, nbins, flags, nullptr, sms, st);
@@ -567,8 +627,24 @@ cudaError_t launch_add_key(uint32_t* keys, uint64_t n, const uint32_t* mm, int s
 // merge_local (vcec.hpp:35-66) + vcec_to_ecc (curve.hpp:28-35) over a dense
 // histogram: occurring bins (count > 0) are compacted in ascending order
 // and their change sums prefix-summed.  Bins that never occur have a zero
-// change sum, so chi at an occurring bin is the prefix over all bins.
+// change sum, so chi at an occurring bin is the prefix over all bins.  The
+// histogram is int64[2][nbins] (sums, counts) or, PACKED, the generic
+// kernels' uint64[nbins] words count << 32 | sum(change + 8).
+template <bool PACKED>
+__device__ __forceinline__ void bin_at(const int64_t* __restrict__ hist, uint32_t nbins, uint32_t b,
+                                       long long& sum, long long& cnt) {
+  if constexpr (PACKED) {
+    const unsigned long long w = (unsigned long long)hist[b];
+    cnt = (long long)(w >> 32);
+    sum = (long long)(w & 0xFFFFFFFFull) - 8 * cnt;
+  } else {
+    sum = hist[b];
+    cnt = hist[nbins + b];
+  }
+}
+
 // One CTA of 1024 threads, each owning a contiguous run of bins.
+template <bool PACKED>
 __global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ hist,
                                                    uint32_t nbins, uint32_t* bins,
                                                    int64_t* changes, int64_t* chi,
@@ -580,8 +656,10 @@ __global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ h
   const uint32_t b1 = min(nbins, b0 + per);
   long long npres = 0, sum = 0;
   for (uint32_t b = b0; b < b1; ++b) {
-    npres += hist[nbins + b] != 0;
-    sum += hist[b];
+    long long sm, ct;
+    bin_at<PACKED>(hist, nbins, b, sm, ct);
+    npres += ct != 0;
+    sum += sm;
   }
   longlong2 in = make_longlong2(npres, sum), ex;
   struct Add {
@@ -593,10 +671,12 @@ __global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ h
   Scan(tmp).ExclusiveScan(in, ex, make_longlong2(0, 0), Add(), total);
   long long pos = ex.x, acc = ex.y;
   for (uint32_t b = b0; b < b1; ++b) {
-    acc += hist[b];
-    if (hist[nbins + b] != 0) {
+    long long sm, ct;
+    bin_at<PACKED>(hist, nbins, b, sm, ct);
+    acc += sm;
+    if (ct != 0) {
       bins[pos] = b;
-      changes[pos] = hist[b];
+      changes[pos] = sm;
       chi[pos] = acc;
       ++pos;
     }
@@ -604,10 +684,10 @@ __global__ void __launch_bounds__(1024) k_finalize(const int64_t* __restrict__ h
   if (threadIdx.x == 1023) *count = (uint64_t)total.x;
 }
 
-// Large bin counts (65536 for u16 / quantised f32): three small grids --
-// per-1024-bin partial (count, sum), one scan of the partials, and the
-// block-local scan that writes the compacted curve -- instead of one CTA
-// walking all bins.
+// Large bin counts (65536 for u16 / quantised f32, up to 2^24 for the dense
+// sorted-f32 path): three small grids -- per-1024-bin partial (count, sum),
+// one scan of the partials, and the block-local scan that writes the
+// compacted curve -- instead of one CTA walking all bins.
 namespace fin {
 constexpr int T = 256, PER = 4, B = T * PER;
 
@@ -617,6 +697,7 @@ struct Add2 {
   }
 };
 
+template <bool PACKED>
 __global__ void __launch_bounds__(T) k_partials(const int64_t* __restrict__ hist, uint32_t nbins,
                                                 longlong2* __restrict__ part) {
   using Red = cub::BlockReduce<longlong2, T>;
@@ -626,8 +707,10 @@ __global__ void __launch_bounds__(T) k_partials(const int64_t* __restrict__ hist
 #pragma unroll
   for (int i = 0; i < PER; ++i)
     if (b0 + i < nbins) {
-      v.x += hist[nbins + b0 + i] != 0;
-      v.y += hist[b0 + i];
+      long long sm, ct;
+      bin_at<PACKED>(hist, nbins, b0 + i, sm, ct);
+      v.x += ct != 0;
+      v.y += sm;
     }
   const longlong2 t = Red(tmp).Reduce(v, Add2());
   if (threadIdx.x == 0) part[blockIdx.x] = t;
@@ -651,19 +734,19 @@ __global__ void __launch_bounds__(1024) k_scan_partials(longlong2* part, uint32_
   if (threadIdx.x == 0) *count = (uint64_t)total.x;
 }
 
+template <bool PACKED>
 __global__ void __launch_bounds__(T) k_write(const int64_t* __restrict__ hist, uint32_t nbins,
                                              const longlong2* __restrict__ part, uint32_t* bins,
                                              int64_t* changes, int64_t* chi) {
   using Scan = cub::BlockScan<longlong2, T>;
   __shared__ typename Scan::TempStorage tmp;
   const uint32_t b0 = blockIdx.x * B + threadIdx.x * PER;
-  int64_t s[PER], n[PER];
+  long long s[PER], n[PER];
   longlong2 v = make_longlong2(0, 0);
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const bool in = b0 + i < nbins;
-    s[i] = in ? hist[b0 + i] : 0;
-    n[i] = in ? hist[nbins + b0 + i] : 0;
+    s[i] = n[i] = 0;
+    if (b0 + i < nbins) bin_at<PACKED>(hist, nbins, b0 + i, s[i], n[i]);
     v.x += n[i] != 0;
     v.y += s[i];
   }
@@ -685,16 +768,25 @@ __global__ void __launch_bounds__(T) k_write(const int64_t* __restrict__ hist, u
 
 cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
                             int64_t* changes, int64_t* chi, uint64_t* count, void* scratch,
-                            cudaStream_t st) {
+                            cudaStream_t st, bool packed) {
   if (nbins <= 4096 || !scratch) {
-    k_finalize<<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
+    if (packed)
+      k_finalize<true><<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
+    else
+      k_finalize<false><<<1, 1024, 0, st>>>(hist, nbins, bins, changes, chi, count);
     return cudaGetLastError();
   }
   const uint32_t nblk = (nbins + fin::B - 1) / fin::B;  // scratch: nblk x 16 bytes
   longlong2* part = static_cast<longlong2*>(scratch);
-  fin::k_partials<<<nblk, fin::T, 0, st>>>(hist, nbins, part);
+  if (packed)
+    fin::k_partials<true><<<nblk, fin::T, 0, st>>>(hist, nbins, part);
+  else
+    fin::k_partials<false><<<nblk, fin::T, 0, st>>>(hist, nbins, part);
   fin::k_scan_partials<<<1, 1024, 0, st>>>(part, nblk, count);
-  fin::k_write<<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi);
+  if (packed)
+    fin::k_write<true><<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi);
+  else
+    fin::k_write<false><<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi);
   return cudaGetLastError();
 }
 

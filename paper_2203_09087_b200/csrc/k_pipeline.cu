@@ -107,10 +107,17 @@ __global__ void __launch_bounds__(ROW_T)
 // so the load latency hides behind the taps (widths up to 64).
 constexpr int UPB = 8;
 
+// mm != nullptr (the last pass of a smoothing whose result is ECC'ed next):
+// also reduce the outputs' order-key range into mm[0] (min) / mm[1] (max)
+// and raise kFlagNaN in *flags -- the key-range pass of the sorted-f32 ECC,
+// fused (the values are in registers here anyway).
 template <int J>
 __global__ void __launch_bounds__(ROW_T)
     k_smooth_rows_p(const float* __restrict__ in, float* __restrict__ out, uint32_t L,
-                    uint32_t tiles, uint64_t units, const double* __restrict__ w, int width) {
+                    uint32_t tiles, uint64_t units, const double* __restrict__ w, int width,
+                    uint32_t* __restrict__ mm, uint32_t* __restrict__ flags) {
+  uint32_t klo = 0xFFFFFFFFu, khi = 0;
+  bool nan = false;
   constexpr int ROW_OUT = ROW_T * J, NV = (ROW_OUT + 63 + ROW_T - 1) / ROW_T;
   extern __shared__ double sh[];
   double* ws = sh;          // [width]
@@ -158,8 +165,26 @@ __global__ void __launch_bounds__(ROW_T)
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const int64_t p = p0 + threadIdx.x + ROW_T * j;
-      if (p < (int64_t)L) dst[p] = __double2float_rn(acc[j]);
+      if (p < (int64_t)L) {
+        const float f = __double2float_rn(acc[j]);
+        dst[p] = f;
+        if (mm) {
+          const uint32_t kk = float_order_key_bits(__float_as_uint(f));
+          klo = min(klo, kk);
+          khi = max(khi, kk);
+          nan |= f != f;
+        }
+      }
     }
+  }
+  if (mm) {
+    klo = __reduce_min_sync(0xFFFFFFFFu, klo);
+    khi = __reduce_max_sync(0xFFFFFFFFu, khi);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(mm, klo);
+      atomicMax(mm + 1, khi);
+    }
+    if (nan) atomicOr(flags, kFlagNaN);
   }
 }
 
@@ -311,7 +336,8 @@ int gaussian_max_width() { return pipe::MAXW; }
 
 cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint64_t w1,
                                  uint64_t w2, int axis, const double* d_weights, int width,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, uint32_t* mm, uint32_t* flags, bool* ranged) {
+  if (ranged) *ranged = false;
   using namespace pipe;
   const uint64_t ext[3] = {w0, w1, w2};
   const uint64_t L = ext[axis];
@@ -362,8 +388,9 @@ cudaError_t launch_convolve_axis(const float* in, float* out, uint64_t w0, uint6
         if (smem > 48 * 1024)
           cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, ROW_T, smem, st>>>(in, out, (uint32_t)L, (uint32_t)tiles, units, d_weights,
-                                        width);
+                                        width, mm, flags);
       };
+      if (ranged) *ranged = mm != nullptr;
       if (J == 1)
         go(k_smooth_rows_p<1>);
       else if (J == 2)
