@@ -49,6 +49,25 @@ def test_fused_exchange_timeout_fails_loudly():
     assert "TIMEOUT OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
+def test_fused_exchange_peer_process_killed():
+    """A rank's process is SIGKILLed mid-run: the surviving rank's next fused
+    launch must fail with ECC_ECUDA (timed out), a poisoned count, and not
+    hang.  The two ranks are started directly (torchrun would tear the
+    survivor down as soon as a worker dies)."""
+    port = _port()
+    procs = []
+    for rank in range(2):
+        env = dict(os.environ, RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE="2",
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tools",
+                                                                    "xchg_timeout_check.py"),
+                                       "--kill"], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=300) for p in procs]
+    assert procs[1].returncode == -9, outs[1][1][-2000:]  # the killed rank
+    assert procs[0].returncode == 0 and "KILL OK" in outs[0][0], outs[0][0][-2000:] + outs[0][1][-2000:]
+
+
 def test_bench_two_ranks_self_launch():
     """`python bench.py --gpus 2` without torchrun re-launches itself with one
     process per rank; on a one-GPU box the ranks share the device over gloo.

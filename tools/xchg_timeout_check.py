@@ -5,9 +5,14 @@ poisoned, ecc_xchg_status fails with ECC_ECUDA, and every later
 ecc_curve_sharded call on that exchange fails too (its step count is out of
 step with its peers).  Runs as 2 processes on one GPU (CUDA IPC).
 
-  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/xchg_timeout_check.py
+  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/xchg_timeout_check.py [--kill]
+
+--kill: rank 1's PROCESS is killed (SIGKILL) before the second step instead
+of merely skipping it; rank 0 must still get ECC_ECUDA, a poisoned count and
+no hang (no collective runs after the kill).
 """
 import os
+import signal
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -54,15 +59,24 @@ def main():
     m = int(cnt.item())
     ok = np.array_equal(chg[:m].cpu().numpy(), c)
     dist.barrier()
+    kill = "--kill" in sys.argv
+    if kill and rank == 1:
+        torch.cuda.synchronize()
+        os.kill(os.getpid(), signal.SIGKILL)  # a rank dies mid-run
     result = "ok"
     if rank == 0:
-        launch()  # step 2: rank 1 is "dead" -> times out after 10 s
+        if kill:
+            import time
+            time.sleep(2.0)  # the peer is gone before this step starts
+        launch()  # step 2: rank 1 is dead -> times out after 10 s
         try:
             x.status()
             result = "status did not fail"
         except eb.EccError as e:
             if "timed out" not in str(e):
                 result = f"wrong error: {e}"
+            elif e.code != -2:  # ECC_ECUDA
+                result = f"wrong error code {e.code}"
         if result == "ok" and int(cnt.item()) != -1:  # ~0ull read as int64
             result = f"count not poisoned: {int(cnt.item())}"
         if result == "ok":
@@ -72,6 +86,12 @@ def main():
             except eb.EccError as e:
                 if "timed out" not in str(e):
                     result = f"wrong error on the next call: {e}"
+    if kill:  # no collectives with a dead peer
+        tag = "KILL"
+        print(f"{tag} OK" if (ok and result == "ok") else f"{tag} FAILED: {result} step1={ok}",
+              flush=True)
+        x.close()
+        os._exit(0)
     dist.barrier()
     if rank == 0:
         print("TIMEOUT OK" if (ok and result == "ok") else f"TIMEOUT FAILED: {result} step1={ok}",
