@@ -58,7 +58,9 @@ __device__ __forceinline__ uint64_t globaltimer() {
 //       static __device__ bool live(int c) (a real change, not "not emitted");
 //       static __device__ int change(int c).
 // ghist: [256] change sums then [256] pixel counts.
-template <int NT, class Code>
+// REP: the table is replicated REP times (entry e at words e * REP .. + REP-1,
+// one replica per group of 32 / REP lanes, to spread the shared-memory banks).
+template <int NT, class Code, int REP = 1>
 __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t* ghist,
                                                    const Fin& fin) {
   static_assert(256 % NT == 0 || NT % 256 == 0, "NT must divide 256 or be a multiple of it");
@@ -68,7 +70,9 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
 #pragma unroll
     for (int c = 0; c < Code::n; ++c) {
       if (!Code::live(c)) continue;
-      const long long n = hist[c * 256 + v];
+      long long n = 0;
+#pragma unroll
+      for (int r = 0; r < REP; ++r) n += hist[(c * 256 + v) * REP + r];
       cnt += n;
       sum += n * Code::change(c);
     }

@@ -62,7 +62,7 @@ namespace u83d {
 using u8fin::flush_and_finalize;
 
 #ifndef ECC_U83D_NW
-#define ECC_U83D_NW 8
+#define ECC_U83D_NW 16
 #endif
 constexpr int NW = ECC_U83D_NW;  // warps per CTA
 #ifndef ECC_U83D_NS
@@ -78,12 +78,16 @@ constexpr int BOXY = 32;   // rows per box (one per lane)
 constexpr int PLANE_BYTES = BOXZ * BOXY;
 constexpr int STAGE = PLANE_BYTES * PB;
 constexpr int NCODE = 16;
-constexpr int HIST_WORDS = NCODE * 256;
+#ifndef ECC_U83D_HREP
+#define ECC_U83D_HREP 4
+#endif
+constexpr int HREP = ECC_U83D_HREP;  // histogram replicas (one per 32 / HREP lanes: fewer bank conflicts)
+constexpr int HIST_WORDS = NCODE * 256 * HREP;
 constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + HIST_WORDS * 4;
 #ifndef ECC_U83D_CTAS
-#define ECC_U83D_CTAS 2
+#define ECC_U83D_CTAS 1
 #endif
 constexpr int CTAS_PER_SM = ECC_U83D_CTAS;
 constexpr uint32_t FULL = 0xFFFFFFFFu;
@@ -421,7 +425,8 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
   XCarry xc;
   RunGeom rg;
   uint32_t step = 0;
-  const uint32_t hist_s = smem_u32(hist);
+  // this lane's replica of the table: entry e at word e * HREP + replica
+  const uint32_t hist_s = smem_u32(hist) + (uint32_t)((lane * HREP) >> 5) * 4u;
   for (int u = gw; u < g.nunits; u += nwt) {
     Cursor cc;
     cc.start(g, u);
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
     if (X <= x0 + len)  // odd plane count: the last box's second plane is unused
       sweep_step<CH, 2, 0, true>(g, X, zs, rg, step, myring, myfull, hist_s, pc, lane, B, A, xc, issue);
   }
-  if constexpr (!CH) flush_and_finalize<NW * 32, Codes>(hist, ghist, fin);
+  if constexpr (!CH) flush_and_finalize<NW * 32, Codes, HREP>(hist, ghist, fin);
 }
 
 }  // namespace u83d
@@ -514,7 +519,7 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.Gz = (g.W2 + 29) / 30;
   g.ncols = g.Gy * g.Gz;
   g.chg = chg;
-  g.four = 4;
+  g.four = 4 * HREP;
   smem_optin<k_u8_3d<false>>(SMEM_BYTES);
   smem_optin<k_u8_3d<true>>(SMEM_BYTES);
   static int per_sm = -1;  // same on every B200
