@@ -275,15 +275,15 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
       const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;
       const uint32_t I[9] = {FULL, Z1, Z0, gyu, ~P.gy, (P.gz & gyzu) << 1, Z0 & gyzu,
                              (P.gz & ~P.gyz) << 1, Z0 & ~P.gyz};
-      const uint32_t X[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
+      const uint32_t Xn[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
       const uint32_t Xp[9] = {xc.gxa, xc.gxz1, xc.gxz, xc.gxyu, xc.gxy,
                               xc.g8u1, xc.g8u, xc.g81, xc.g8};
       uint32_t h[9], l[9];
 #pragma unroll
       for (int b = 0; b < 9; ++b) {
-        l[b] = bits::lop3<0x9F>(I[b], X[b], Xp[b]);  // ~(I & (X ^ Xp))
-        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], X[b], Xp[b])   // I & X & ~Xp
-                                  : bits::lop3<0x20>(I[b], X[b], Xp[b]);  // I & ~X & Xp
+        l[b] = bits::lop3<0x9F>(I[b], Xn[b], Xp[b]);  // ~(I & (X ^ Xp))
+        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], Xn[b], Xp[b])   // I & X & ~Xp
+                                  : bits::lop3<0x20>(I[b], Xn[b], Xp[b]);  // I & ~X & Xp
       }
       // S = change + 9; change = S + 7 mod 16 in 4-bit two's complement
       uint32_t s[4];

@@ -332,7 +332,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
                              Z0 & ~P.gyz};
       // X_b: the next plane's copy of b beats this plane's; Xp_b the same
       // one step earlier (the previous plane against this one)
-      const uint32_t X[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
+      const uint32_t Xn[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
       const uint32_t Xp[9] = {xc.gxa, xc.gxz1, xc.gxz, xc.gxyu, xc.gxy,
                               xc.g8u1, xc.g8u, xc.g81, xc.g8};
       // q_b = 1 + s_b I_b (X_b - Xp_b) in {0, 1, 2} as 2 h_b + l_b (signs:
@@ -340,9 +340,9 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
       uint32_t h[9], l[9];
 #pragma unroll
       for (int b = 0; b < 9; ++b) {
-        l[b] = bits::lop3<0x9F>(I[b], X[b], Xp[b]);  // ~(I & (X ^ Xp))
-        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], X[b], Xp[b])   // I & X & ~Xp
-                                  : bits::lop3<0x20>(I[b], X[b], Xp[b]);  // I & ~X & Xp
+        l[b] = bits::lop3<0x9F>(I[b], Xn[b], Xp[b]);  // ~(I & (X ^ Xp))
+        h[b] = (b >= 1 && b <= 4) ? bits::lop3<0x40>(I[b], Xn[b], Xp[b])   // I & X & ~Xp
+                                  : bits::lop3<0x20>(I[b], Xn[b], Xp[b]);  // I & ~X & Xp
       }
       // S = change + 9 in [2, 14]; code = S mod 16; not emitted -> 15
       uint32_t s[4];
@@ -357,7 +357,8 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
           const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
                                           (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
           if ((vm >> p) & 1) {
-            const long long vox = ((long long)(X - 1 - g.own0) * g.W1 + rg.y) * g.W2 + (zs - 1) + p;
+            const long long row = (long long)(X - 1 - g.own0) * g.W1 + rg.y;
+            const long long vox = row * g.W2 + (long long)(zs - 1 + p);
             g.chg[vox] = (int8_t)decode_change(idx >> 8);
           }
         }

@@ -194,13 +194,25 @@ def test_slabs_sum_to_whole(ctx):
 def test_compute_changes_matches_oracle(ctx):
     import torch
     rng = np.random.default_rng(9)
-    for shape in [(20, 21, 22), (30, 40, 1)]:
-        img = rng.integers(0, 5, shape).astype(np.uint8)
+    # (24, 40, 48) / (17, 35, 64) / (40, 70, 96): rows a multiple of 16 bytes -> the TMA-fed
+    # bit-sliced kernel's changes mode; (20, 21, 22) -> the tournament kernel; (30, 40, 1) 2D
+    for shape, hi in [((20, 21, 22), 5), ((30, 40, 1), 5), ((24, 40, 48), 5), ((17, 35, 64), 256),
+                      ((40, 70, 96), 3)]:
+        img = rng.integers(0, hi, shape).astype(np.uint8)
         dev = torch.from_numpy(img).cuda()
-        out = torch.empty(img.size, dtype=torch.int8, device="cuda")
+        out = torch.full((img.size,), 99, dtype=torch.int8, device="cuda")
         ctx.compute_changes(dev, eb.Dims.of(shape), 0, 0, shape[0], out)
         torch.cuda.synchronize()
-        assert np.array_equal(out.cpu().numpy().reshape(shape), oracle.changes(img))
+        assert np.array_equal(out.cpu().numpy().reshape(shape), oracle.changes(img)), shape
+    # a slab of the TMA-shaped volume: owned planes [5, 19) with their halo planes only
+    shape = (24, 40, 48)
+    img = rng.integers(0, 7, shape).astype(np.uint8)
+    want = oracle.changes(img)[5:19]
+    slab = torch.from_numpy(np.ascontiguousarray(img[4:20])).cuda()
+    out = torch.full((14 * 40 * 48,), 99, dtype=torch.int8, device="cuda")
+    ctx.compute_changes(slab, eb.Dims.of(shape), 4, 5, 19, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().reshape(want.shape), want)
 
 
 def test_stream_failure_names_chunk(ctx):
