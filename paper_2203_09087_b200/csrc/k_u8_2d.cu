@@ -25,7 +25,7 @@
 // [-3, 1].  S = change + 3 (8 win bits through a small carry-save adder) is
 // the code; the three code planes are transposed back to bytes and every
 // pixel does ONE shared-memory red at hist[code][value].  Pixels the lane
-// does not emit get code 15.
+// does not emit get code 7.
 //
 // Collar.  Pixels outside the image hold 255; only an outside pixel on the
 // EARLIER side of a comparison is wrong (the reference's sentinel 256 must
@@ -42,11 +42,21 @@
 namespace eccb {
 namespace u82d {
 
-constexpr int NW = 8;  // warps per CTA
+#ifndef ECC_U82D_NW
+#define ECC_U82D_NW 16
+#endif
+#ifndef ECC_U82D_CTAS
+#define ECC_U82D_CTAS 1
+#endif
+#ifndef ECC_U82D_HREP
+#define ECC_U82D_HREP 4
+#endif
+constexpr int NW = ECC_U82D_NW;  // warps per CTA
 constexpr int NT = NW * 32;
-constexpr int NCODE = 16;
-constexpr int HIST_WORDS = NCODE * 256;
-constexpr int CTAS_PER_SM = 2;
+constexpr int NCODE = 8;         // S = change + 3 in [0, 4]; 7 = not emitted
+constexpr int HREP = ECC_U82D_HREP;  // table replicas, one per 32 / HREP lanes (bank spread)
+constexpr int HIST_WORDS = NCODE * 256 * HREP;
+constexpr int CTAS_PER_SM = ECC_U82D_CTAS;
 constexpr int STRIP = 30;  // owned chunks per warp
 constexpr uint32_t FULL = 0xFFFFFFFFu;
 
@@ -100,7 +110,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwt = gridDim.x * NW;
-  const uint32_t hist_s = smem_u32(hist);
+  const uint32_t hist_s = smem_u32(hist) + (uint32_t)(((threadIdx.x & 31) * HREP) >> 5) * 4u;
 
   for (int u = blockIdx.x * NW + warp; u < g.nunits; u += nwt) {
     const int bi = u / g.nstrips, strip = u - bi * g.nstrips;
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
             const uint32_t b2 = k1 ^ k1x;               // weight 4 (S <= 4)
             const uint32_t nv = ~vmr;
             uint32_t V[8];
-            bits::transpose_codes(b0 | nv, b1x | nv, b2 | nv, nv, V);
+            bits::transpose_codes(b0 | nv, b1x | nv, b2 | nv, 0u, V);
 #pragma unroll
             for (int p = 0; p < 32; ++p) {
               const int r = p & 7, b = p >> 3;
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
   }
-  u8fin::flush_and_finalize<NT, Codes>(hist, ghist, fin);
+  u8fin::flush_and_finalize<NT, Codes, HREP>(hist, ghist, fin);
 }
 
 }  // namespace u82d
@@ -240,7 +250,7 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   g.P = (int)(s.own1 - s.own0);
   g.nchunks = (g.W1 + 31) / 32;
   g.nstrips = (g.nchunks + STRIP - 1) / STRIP;
-  g.four = 4;
+  g.four = 4 * HREP;
   const long long cap_warps = (long long)sms * CTAS_PER_SM * NW;
   // bands of >= 32 rows (2 halo rows per band); ~4 units per resident warp
   // when the image is large enough, else one wave of shorter bands (>= MINBAND:
