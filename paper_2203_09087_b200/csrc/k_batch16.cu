@@ -37,6 +37,9 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 #define ECC_HGRP 8
 #endif
 constexpr int HGRP = ECC_HGRP;  // pixels per atomic group (divides 32)
+#ifndef ECC_B16_ASYNC
+#define ECC_B16_ASYNC 1
+#endif
 static_assert(hist16::no_wrap(NT, HGRP, 3), "2D changes reach -3: the packed halves could wrap");
 constexpr uint32_t BIAS = 0x80008000u;
 
@@ -104,6 +107,53 @@ __global__ void __launch_bounds__(NT, 1)
   const bool vec = (w & 7) == 0;
   const uint32_t hbase = smem_u32(hw), pbase = smem_u32(pres);
 
+#if ECC_B16_ASYNC
+  // the next row is staged in shared memory by cp.async (no registers held
+  // for it across the step): two slots per thread, slot = row parity
+  uint32_t* stage = spilled + PWORDS;  // [2][NT][16] words
+  auto issue_row = [&](int i) {
+    uint32_t* dst = stage + ((i & 1) * NT + threadIdx.x) * 16;
+    if (i < 0 || i >= h || c >= nchunks) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(dst)[q] = make_uint4(FULL, FULL, FULL, FULL);
+    } else {
+      const uint16_t* p = img + (size_t)i * w + lo;
+      if (vec && w - lo >= 32) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 4 * q)),
+                       "l"(p + 8 * q)
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t a = (lo + 2 * j < w) ? __ldg(p + 2 * j) : 0xFFFFu;
+          const uint32_t b = (lo + 2 * j + 1 < w) ? __ldg(p + 2 * j + 1) : 0xFFFFu;
+          dst[j] = a | (b << 16);
+        }
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto take_row = [&](int i, uint32_t (&W)[16]) {
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // row i landed, row i + 1 in flight
+    const uint4* src = reinterpret_cast<const uint4*>(stage + ((i & 1) * NT + threadIdx.x) * 16);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 v = src[q];
+      W[4 * q] = v.x; W[4 * q + 1] = v.y; W[4 * q + 2] = v.z; W[4 * q + 3] = v.w;
+    }
+  };
+  Row A, B;
+  uint32_t xgx = 0, xgq = 0, xgq1 = 0;  // previous row pair's results
+  issue_row(R0 - 1);
+  // steps: rows R0-1 .. R0+rows arrive; at the arrival of row X the changes
+  // of row X-1 are emitted (X-1 in [R0, R0 + rows) and inside the image)
+  auto step = [&](int X, Row& P, Row& N, auto kind) {
+    constexpr int K = decltype(kind)::value;  // 0 first, 1 no emission, 2 emit
+    issue_row(X + 1);  // prefetch (collar past the band's last row + 1 is harmless)
+    take_row(X, N.W);
+#else
   auto load_row = [&](int i, uint32_t (&W)[16]) {
     if (i < 0 || i >= h || c >= nchunks) {
 #pragma unroll
@@ -138,6 +188,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
     for (int j = 0; j < 16; ++j) N.W[j] = nxt[j];
     load_row(X + 1, nxt);  // prefetch (collar past the band's last row + 1 is harmless)
+#endif
     planes16(N.W, N.C);
     const bool xout = X < 0 || X >= h;
     const uint32_t om = xout ? FULL : zout;
@@ -306,7 +357,7 @@ cudaError_t launch_batch16(const uint16_t* data, uint64_t count, int h, int w, i
   if (count == 0) return cudaSuccess;
   int L = 1;
   while (L < (w + 31) / 32) L <<= 1;
-  const size_t smem = (size_t)(HWORDS + 2 * PWORDS) * 4;
+  const size_t smem = (size_t)(HWORDS + 2 * PWORDS + (ECC_B16_ASYNC ? 2 * NT * 16 : 0)) * 4;
   smem_optin<k_batch16>((int)smem);
   k_batch16<<<(unsigned)count, NT, smem, st>>>(data, h, w, L, chi, presence, spill_scratch);
   return cudaGetLastError();
