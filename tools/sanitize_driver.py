@@ -61,6 +61,26 @@ for b in range(3):
     good = np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
     ok &= good
     print(("ok  " if good else "BAD ") + f"batch2d u16 #{b}", flush=True)
+imgsv = rng.integers(0, 65536, (2, 64, 512)).astype(np.uint16)  # C3-shaped rows: cp.async staging
+chi, pres = ctx.batch2d(imgsv)
+for b in range(2):
+    t, cc = eb.curve_batch_to_points(chi[b], pres[b])
+    v, c = oracle.vcec(imgsv[b])
+    good = np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
+    ok &= good
+    print(("ok  " if good else "BAD ") + f"batch2d u16 512-wide #{b}", flush=True)
+# general f32 over >= 2^20 voxels with a narrow key span: the packed dense histogram
+fd = (0.5 + rng.random((64, 128, 128)) * 1e-3).astype(np.float32)
+check("f32 sorted dense packed", ctx.vcec(torch.from_numpy(fd).cuda()), fd)
+# TMA-shaped u8 compute_changes (the bit-sliced kernel's changes mode)
+img = rng.integers(0, 9, (10, 40, 48)).astype(np.uint8)
+dev = torch.from_numpy(img).cuda()
+out = torch.empty(img.size, dtype=torch.int8, device="cuda")
+ctx.compute_changes(dev, eb.Dims.of(img.shape), 0, 0, 10, out)
+torch.cuda.synchronize()
+good = np.array_equal(out.cpu().numpy().reshape(img.shape), oracle.changes(img))
+ok &= good
+print(("ok  " if good else "BAD ") + "compute_changes u8 TMA-shaped", flush=True)
 imgs8 = rng.integers(0, 256, (3, 31, 45)).astype(np.uint8)
 chi, pres = ctx.batch2d(imgs8)
 t, cc = eb.curve_batch_to_points(chi[1], pres[1])
