@@ -109,6 +109,22 @@ void batch2d(const T* images, std::uint64_t count, std::uint64_t h, std::uint64_
                             chi.data(), presence.data(), nullptr));
 }
 
+// write_curve's CSV / JSON text (curve.hpp:87-121) of one curve, formatted on
+// the GPU (f32 thresholds as std::to_chars' shortest round-trip text):
+// byte-identical to ecc::write_curve, for large curves.
+template <class T>
+std::string format_curve(const EccCurve<T>& c, CurveFormat format, Context& ctx = Context::on(0)) {
+  std::uint64_t n = 0;
+  const int mode = format == CurveFormat::json ? 1 : 0;
+  const int rc = ecc_format_curve(ctx.get(), detail::dtype_of<T>::value, c.thresholds.data(),
+                                  c.chi.data(), c.size(), 0, mode, nullptr, 0, &n);
+  if (rc != ECC_OK && n == 0) detail::check(rc);
+  std::string out(n, '\0');
+  detail::check(ecc_format_curve(ctx.get(), detail::dtype_of<T>::value, c.thresholds.data(),
+                                 c.chi.data(), c.size(), 0, mode, out.data(), n, &n));
+  return out;
+}
+
 // Occurring points of one dense batched curve row.
 template <class T>
 EccCurve<T> batch_row_curve(const std::int32_t* chi_row, const std::uint32_t* presence_row,

@@ -396,6 +396,18 @@ ECC_API int ecc_gaussian_smooth_host(ecc_ctx* ctx, const float* in, float* out, 
 ECC_API int ecc_fixup_f32_host(ecc_ctx* ctx, float* data, uint64_t n, uint64_t base,
                                int big_endian);
 
+/* ------------------------------------------------------------ one curve's text on the device
+ * write_curve (curve.hpp:87-121; mode 0 CSV, 1 JSON) or write_vcec
+ * (curve.hpp:154-169; mode 2) of ONE curve / VCEC, formatted on the GPU and
+ * byte-identical to the reference writers: thresholds / values of dtype
+ * (u8 / u16 integers; f32 as the shortest round-trip text std::to_chars
+ * prints, format_value curve.hpp:56-66) and int64 chi / changes, n points,
+ * host (where = 0) or device (where = 1) arrays.  `out` (host) receives the
+ * bytes; *size_out = their count (also when it exceeds cap, with ECC_EINVAL). */
+ECC_API int ecc_format_curve(ecc_ctx* ctx, ecc_dtype dtype, const void* thresholds,
+                             const int64_t* chi, uint64_t n, int where, int mode, char* out,
+                             uint64_t cap, uint64_t* size_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -117,6 +117,9 @@ def lib() -> C.CDLL:
             L.ecc_batch_format.argtypes = [_vp, _vp, _vp, _u64, C.c_int, C.c_int, _vp, _u64,
                                            _vp, C.POINTER(_u64)]
             L.ecc_batch_format.restype = C.c_int
+            L.ecc_format_curve.argtypes = [_vp, C.c_int, _vp, _vp, _u64, C.c_int, C.c_int, _vp, _u64,
+                                           C.POINTER(_u64)]
+            L.ecc_format_curve.restype = C.c_int
             L.ecc_batch_zero_crossings.argtypes = [_vp, _vp, _vp, _u64, C.c_int, _vp, _vp]
             L.ecc_batch_zero_crossings.restype = C.c_int
             L.ecc_xchg_create.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_vp), _vp]
@@ -757,6 +760,31 @@ class Context:
         _check(lib().ecc_batch_format(self._p, chi.data_ptr(), presence.data_ptr(), count, dt, f,
                                       out.ctypes.data, out.size, offs.ctypes.data, C.byref(total)))
         return [out[int(offs[i]):int(offs[i + 1])].tobytes() for i in range(count)]
+
+    def format_curve(self, thresholds, chi, fmt: str = "csv") -> bytes:
+        """write_curve (fmt "csv" / "json", curve.hpp:87-121) or write_vcec
+        ("vcec": values + changes, curve.hpp:154-169) bytes of ONE curve,
+        formatted on the GPU -- f32 thresholds as std::to_chars' shortest
+        round-trip text.  numpy arrays or CUDA tensors."""
+        mode = {"csv": 0, "json": 1, "vcec": 2}[fmt]
+        dev = hasattr(thresholds, "data_ptr")
+        if dev:
+            import torch
+            dt = {torch.uint8: np.uint8, torch.uint16: np.uint16, torch.float32: np.float32}[thresholds.dtype]
+            tp, cp, n = thresholds.data_ptr(), chi.data_ptr(), thresholds.numel()
+        else:
+            thresholds = np.ascontiguousarray(thresholds)
+            chi = np.ascontiguousarray(chi, dtype=np.int64)
+            dt, tp, cp, n = thresholds.dtype, thresholds.ctypes.data, chi.ctypes.data, thresholds.size
+        total = _u64()
+        rc = lib().ecc_format_curve(self._p, _DT[np.dtype(dt)], tp, cp, n, 1 if dev else 0, mode,
+                                    None, 0, C.byref(total))
+        if rc != 0 and total.value == 0:
+            _check(rc)
+        out = np.empty(max(1, total.value), np.uint8)
+        _check(lib().ecc_format_curve(self._p, _DT[np.dtype(dt)], tp, cp, n, 1 if dev else 0, mode,
+                                      out.ctypes.data, out.size, C.byref(total)))
+        return out[:total.value].tobytes()
 
     def batch_zero_crossings(self, chi, presence, dtype=np.uint16, out=None, stream: int = 0):
         """zero_crossings (curve.hpp:36-50) of every image of a device batch:

@@ -2351,3 +2351,71 @@ int ecc_fixup_f32_host(ecc_ctx* ctx, float* data, uint64_t n, uint64_t base, int
   if (first != ~0ull) return fail(ECC_ENAN, "NaN value at linear index " + std::to_string(first));
   return ECC_OK;
 }
+
+// ===================================================================== one curve's text
+namespace {
+struct ToU64 {
+  __host__ __device__ uint64_t operator()(uint32_t v) const { return v; }
+};
+}  // namespace
+
+int ecc_format_curve(ecc_ctx* ctx, ecc_dtype dtype, const void* thresholds, const int64_t* chi,
+                     uint64_t n, int where, int mode, char* out, uint64_t cap,
+                     uint64_t* size_out) {
+  CKI(bind(ctx));
+  CKI(check_dtype(dtype));
+  if (!size_out) return fail(ECC_EINVAL, "null size output");
+  if (mode < 0 || mode > 2) return fail(ECC_EINVAL, "format mode must be 0 (CSV), 1 (JSON) or 2 (VCEC CSV)");
+  if (n && (!thresholds || !chi)) return fail(ECC_EINVAL, "null curve arrays");
+  if (n > 0x7FFFFFFFull) return fail(ECC_EINVAL, "curve exceeds 2^31 points");
+  static const char* kHead[3] = {"threshold,euler_characteristic\n", "[", "value,change\n"};
+  static const char* kTail[3] = {"", "]\n", ""};
+  const uint64_t head = std::strlen(kHead[mode]), tail = std::strlen(kTail[mode]);
+  cudaStream_t st = ctx->stream;
+  const void* t = thresholds;
+  const int64_t* c = chi;
+  const size_t es = esize(dtype);
+  if (n && where == 0) {
+    CKI(ctx->input.ensure(n * es));
+    CKI(ctx->asums.ensure(n * 8));
+    CKR(cudaMemcpyAsync(ctx->input.p, thresholds, n * es, cudaMemcpyHostToDevice, st));
+    CKR(cudaMemcpyAsync(ctx->asums.p, chi, n * 8, cudaMemcpyHostToDevice, st));
+    t = ctx->input.p;
+    c = ctx->asums.as<int64_t>();
+  }
+  uint64_t body = 0;
+  if (n) {
+    CKI(ctx->keys2.ensure(n * 4));
+    CKI(ctx->sums2.ensure((n + 1) * 8));
+    CKR(launch_point_sizes(mode, t, (int)dtype, c, n, ctx->keys2.as<uint32_t>(), ctx->sms, st));
+    auto sz = thrust::make_transform_iterator(ctx->keys2.as<const uint32_t>(), ToU64());
+    size_t tb = 0;
+    CKR(cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, ctx->sums2.as<uint64_t>(), (int)n + 0, st));
+    CKI(ctx->tmp.ensure(tb));
+    tb = ctx->tmp.cap;
+    CKR(cub::DeviceScan::ExclusiveSum(ctx->tmp.p, tb, sz, ctx->sums2.as<uint64_t>(), (int)n, st));
+    uint64_t last_off = 0;
+    uint32_t last_sz = 0;
+    CKR(cudaMemcpyAsync(&last_off, ctx->sums2.as<uint64_t>() + (n - 1), 8, cudaMemcpyDeviceToHost, st));
+    CKR(cudaMemcpyAsync(&last_sz, ctx->keys2.as<uint32_t>() + (n - 1), 4, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+    ctx->launches += 2;
+    body = last_off + last_sz;
+  }
+  const uint64_t total = head + body + tail;
+  *size_out = total;
+  if (total > cap || !out)
+    return fail(ECC_EINVAL, "output capacity " + std::to_string(cap) + " < " +
+                                std::to_string(total) + " bytes");
+  std::memcpy(out, kHead[mode], head);
+  if (n) {
+    CKI(ctx->res.ensure(body));
+    CKR(launch_point_write(mode, t, (int)dtype, c, n, ctx->sums2.as<uint64_t>(), 0,
+                           ctx->res.as<char>(), ctx->sms, st));
+    ctx->launches += 1;
+    CKR(cudaMemcpyAsync(out + head, ctx->res.p, body, cudaMemcpyDeviceToHost, st));
+    CKR(cudaStreamSynchronize(st));
+  }
+  std::memcpy(out + head + body, kTail[mode], tail);
+  return ECC_OK;
+}

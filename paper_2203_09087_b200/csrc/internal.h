@@ -109,6 +109,12 @@ cudaError_t launch_format_write(const int32_t* chi, const uint32_t* pres, uint64
                                 cudaStream_t st);
 cudaError_t launch_zero_crossings(const int32_t* chi, const uint32_t* pres, uint64_t count,
                                   uint32_t nbins, uint32_t* zc, cudaStream_t st);
+// one sparse curve's text (k_format.cu): per-point byte counts, then the write
+cudaError_t launch_point_sizes(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                               uint32_t* sizes, int sms, cudaStream_t st);
+cudaError_t launch_point_write(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                               const uint64_t* offsets, uint64_t head, char* out, int sms,
+                               cudaStream_t st);
 cudaError_t launch_fill(void* d, int dtype, uint64_t n, uint64_t seed,
                         uint64_t base, int sms, cudaStream_t st);
 

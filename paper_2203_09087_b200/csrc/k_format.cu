@@ -1,10 +1,11 @@
-// k_format.cu -- curve serialisation on the device for batched curves
-// (SURVEY.md 8(f) rank 4): write_curve's CSV and JSON layouts
-// (curve.hpp:87-121) for every image of a dense batch (ecc_batch2d output:
-// int32 chi[count][nbins] + presence bitmaps), byte-identical to the
-// reference writer.  Thresholds of u8 / u16 curves are integers, so
-// format_value (curve.hpp:56-66) is plain decimal (std::to_chars of an
-// int64); no shortest-float formatting is needed.
+// k_format.cu -- curve serialisation on the device:
+// write_curve's CSV and JSON layouts (curve.hpp:87-121) and write_vcec's CSV
+// (curve.hpp:154-169), byte-identical to the reference writers, for
+//   * every image of a dense batch (ecc_batch2d output: int32
+//     chi[count][nbins] + presence bitmaps; integer thresholds), and
+//   * one sparse curve / VCEC of any value type (u8 / u16 / f32 thresholds,
+//     int64 chi or changes): f32 thresholds through f2s.cuh, the shortest
+//     round-trip text std::to_chars prints (format_value, curve.hpp:56-66).
 //
 // Two passes, one CTA per image: k_format_sizes sums the bytes of the
 // image's occurring points (block reduction); after an exclusive scan over
@@ -12,6 +13,7 @@
 // counts and each thread writes its run of lines.
 #include <cub/cub.cuh>
 
+#include "f2s.cuh"
 #include "internal.h"
 
 namespace eccb {
@@ -215,6 +217,107 @@ cudaError_t launch_format_write(const int32_t* chi, const uint32_t* pres, uint64
                                 cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   fmt::k_format_write<<<(unsigned)count, fmt::NT, 0, st>>>(chi, pres, nbins, json, offsets, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- one sparse curve / VCEC
+namespace fmt1 {
+
+__device__ __forceinline__ int ndigits_u64(uint64_t v) {
+  int n = 1;
+  while (v >= 10) {
+    v /= 10;
+    ++n;
+  }
+  return n;
+}
+
+// text of an int64 (std::to_chars)
+__device__ __forceinline__ int put_i64(char* p, int64_t v) {
+  const bool neg = v < 0;
+  uint64_t a = neg ? (uint64_t)0 - (uint64_t)v : (uint64_t)v;
+  const int n = ndigits_u64(a) + (neg ? 1 : 0);
+  if (p) {
+    int i = n - 1;
+    do {
+      p[i--] = (char)('0' + a % 10);
+      a /= 10;
+    } while (a);
+    if (neg) p[0] = '-';
+  }
+  return n;
+}
+
+// text of threshold i (format_value): integers for u8 / u16, f2s for f32
+__device__ __forceinline__ int put_t(char* p, const void* t, int dtype, uint64_t i) {
+  if (dtype == 2) return f2s::format(__float_as_uint(static_cast<const float*>(t)[i]), p);
+  const int64_t v = dtype == 0 ? (int64_t) static_cast<const uint8_t*>(t)[i]
+                               : (int64_t) static_cast<const uint16_t*>(t)[i];
+  return put_i64(p, v);
+}
+
+// mode 0 CSV curve ("t,chi\n"), 1 JSON curve ("{\"t\":T,\"chi\":C}", comma
+// before all but the first), 2 VCEC CSV ("value,change\n")
+__device__ __forceinline__ int point(char* p, int mode, const void* t, int dtype, const int64_t* c,
+                                     uint64_t i) {
+  int n = 0;
+  if (mode == 1) {
+    if (i) {
+      if (p) p[n] = ',';
+      ++n;
+    }
+    const char* a = "{\"t\":";
+    for (int k = 0; a[k]; ++k, ++n)
+      if (p) p[n] = a[k];
+  }
+  n += put_t(p ? p + n : nullptr, t, dtype, i);
+  if (mode == 1) {
+    const char* b = ",\"chi\":";
+    for (int k = 0; b[k]; ++k, ++n)
+      if (p) p[n] = b[k];
+  } else {
+    if (p) p[n] = ',';
+    ++n;
+  }
+  n += put_i64(p ? p + n : nullptr, c[i]);
+  if (mode == 1) {
+    if (p) p[n] = '}';
+    ++n;
+  } else {
+    if (p) p[n] = '\n';
+    ++n;
+  }
+  return n;
+}
+
+__global__ void k_point_sizes(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                              uint32_t* sizes) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    sizes[i] = (uint32_t)point(nullptr, mode, t, dtype, c, i);
+}
+
+__global__ void k_point_write(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                              const uint64_t* offsets, uint64_t head, char* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    point(out + head + offsets[i], mode, t, dtype, c, i);
+}
+
+}  // namespace fmt1
+
+cudaError_t launch_point_sizes(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                               uint32_t* sizes, int sms, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fmt1::k_point_sizes<<<sms * 4, 256, 0, st>>>(mode, t, dtype, c, n, sizes);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_point_write(int mode, const void* t, int dtype, const int64_t* c, uint64_t n,
+                               const uint64_t* offsets, uint64_t head, char* out, int sms,
+                               cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  fmt1::k_point_write<<<sms * 4, 256, 0, st>>>(mode, t, dtype, c, n, offsets, head, out);
   return cudaGetLastError();
 }
 

@@ -361,6 +361,25 @@ TEST_GPU("FileSource: raw f32 little / big endian, NaN and size errors (chunk.hp
   std::remove(be.c_str());
 } END_TEST
 
+TEST_GPU("device curve text == write_curve (curve.hpp:87-121), f32 thresholds") {
+  std::mt19937 rng(77);
+  EccCurve<float> c;
+  for (int i = 0; i < 3000; ++i) {
+    float v;
+    do {
+      uint32_t u = rng();
+      std::memcpy(&v, &u, 4);
+    } while (!std::isfinite(v));
+    c.thresholds.push_back(v);
+    c.chi.push_back((int64_t)rng() - (int64_t)rng());
+  }
+  for (auto fmtk : {CurveFormat::csv, CurveFormat::json}) {
+    std::ostringstream os;
+    write_curve(c, fmtk, os);
+    CHECK(device::format_curve(c, fmtk) == os.str());
+  }
+} END_TEST
+
 TEST_GPU("bench_run pipeline (pipeline.hpp:236-291) == oracle smoothing + ECC") {
   const Dims d{20, 24, 28};
   const auto rep = bench_run(d, 2, 1, 2.0, 13);

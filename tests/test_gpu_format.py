@@ -87,3 +87,70 @@ def test_batch_zero_crossings(ctx, dt, hi, shape):
         t, c = eb.curve_batch_to_points(chi_h[b], pres_h[b])
         bits = np.unpackbits(zc_h[b].view(np.uint8), bitorder="little").astype(bool)
         assert list(np.nonzero(bits)[0]) == _zero_crossings(t, c), b
+
+
+def _ref_writer_py(t, chi, fmt):
+    """The reference layouts with the thresholds as the reference formats
+    them (oracle.ref_csv for CSV when the reference is compiled)."""
+    import oracle as o
+    def tx(v):
+        if np.issubdtype(np.asarray(t).dtype, np.floating):
+            return repr_float(v)
+        return str(int(v))
+    if fmt == "vcec":
+        return ("value,change\n" + "".join(f"{tx(a)},{int(b)}\n" for a, b in zip(t, chi))).encode()
+    if fmt == "json":
+        return ("[" + ",".join(f'{{"t":{tx(a)},"chi":{int(b)}}}' for a, b in zip(t, chi)) + "]\n").encode()
+    return ("threshold,euler_characteristic\n" +
+            "".join(f"{tx(a)},{int(b)}\n" for a, b in zip(t, chi))).encode()
+
+
+def repr_float(v):
+    """std::to_chars(float) text through the reference's own CSV writer (one
+    point), which is the ground truth for the layout and the digits."""
+    line = oracle.ref_csv(np.array([v], np.float32), np.array([0], np.int64)).decode()
+    return line.split("\n")[1].split(",")[0]
+
+
+@pytest.mark.parametrize("fmt", ["csv", "json", "vcec"])
+def test_format_curve_f32_matches_reference_writer(ctx, fmt):
+    """One f32 curve formatted on the GPU (ecc_format_curve; f2s.cuh is the
+    shortest round-trip formatter) equals the reference's writer byte for
+    byte: awkward magnitudes, subnormals, -0, integers beyond 2^24 (printed
+    exactly), and a smoothed volume's real curve."""
+    import torch
+    if not oracle.ref_available():
+        pytest.skip("reference not compiled here")
+    rng = np.random.default_rng(11)
+    t = np.concatenate([
+        rng.random(500).astype(np.float32) * np.float32(10.0) ** rng.integers(-40, 38, 500).astype(np.float32),
+        np.array([0.0, -0.0, 1e-45, 1.17549435e-38, 1.5258789e-05, 0.0001, 0.001, 123456.0, 1e7,
+                  16777216.0, 50331648.0, 1.2e6, 3.4028235e38, -2.5], np.float32)])
+    t = t[np.isfinite(t)]
+    chi = rng.integers(-2 ** 40, 2 ** 40, t.size)
+    got = ctx.format_curve(t, chi, fmt)
+    if fmt == "csv":
+        assert got == oracle.ref_csv(t, chi)
+    else:
+        assert got == _ref_writer_py(t, chi, fmt)
+    # the device-array path and a real curve of a smoothed field
+    x = torch.empty((24, 30, 36), dtype=torch.float32, device="cuda")
+    ctx.uniform_noise(x, seed=4)
+    y = ctx.gaussian_smooth(x, 1.5, 5)
+    cur = ctx.curve(y.cpu().numpy())
+    dev_t = torch.from_numpy(np.ascontiguousarray(cur.thresholds)).cuda()
+    dev_c = torch.from_numpy(np.ascontiguousarray(cur.chi)).cuda()
+    got = ctx.format_curve(dev_t, dev_c, fmt)
+    if fmt == "csv":
+        assert got == oracle.ref_csv(cur.thresholds, cur.chi)
+    else:
+        assert got == _ref_writer_py(cur.thresholds, cur.chi, fmt)
+
+
+def test_format_curve_integer_thresholds(ctx):
+    img = oracle.synth("u8", (64, 64), seed=2)
+    cur = ctx.curve(img)
+    assert ctx.format_curve(cur.thresholds, cur.chi, "csv") == oracle.ref_csv(cur.thresholds, cur.chi)
+    t16 = np.array([0, 7, 65535], np.uint16)
+    assert ctx.format_curve(t16, np.array([1, -2, 3]), "json") == b'[{"t":0,"chi":1},{"t":7,"chi":-2},{"t":65535,"chi":3}]\n'
+    assert ctx.format_curve(np.zeros(0, np.float32), np.zeros(0, np.int64), "json") == b"[]\n"

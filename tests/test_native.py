@@ -83,3 +83,12 @@ def test_reference_tests_compile_against_the_drop_in():
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
     for t in ["test_streaming", "test_kernel", "test_value_index", "test_curve", "acceptance"]:
         assert os.path.exists(os.path.join(BIN, "ref_" + t)), t
+
+
+def test_f2s_matches_to_chars():
+    """csrc/f2s.cuh (the GPU's float formatter) == std::to_chars(float) on
+    special values, every exponent's extremes, 4 M random bit patterns and
+    decimal-looking values (`tests/cpp/bin/test_f2s all` checks all 2^32
+    floats: profiles/r02v_f2s_all_floats.log)."""
+    out = _run([_bin("test_f2s")])
+    assert "f2s ok" in out
