@@ -63,7 +63,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 template <int NT, class Code, int REP = 1>
 __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t* ghist,
                                                    const Fin& fin) {
-  static_assert(256 % NT == 0 || NT % 256 == 0, "NT must divide 256 or be a multiple of it");
+  static_assert(256 % NT == 0 || NT >= 256, "NT must divide 256 or be at least 256");
   __syncthreads();
   for (int v = threadIdx.x; v < 256; v += NT) {
     long long sum = 0, cnt = 0;
