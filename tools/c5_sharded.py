@@ -87,10 +87,21 @@ def main():
         t = float(tt[0])
     m = int(cnt.item())
     ok = int(chi[m - 1].item()) == 1
+    # the full 4096^3 curve against the reference engine's digest (golden.json C5_full)
+    golden_ok = None
+    if S == 4096:
+        import hashlib
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))["configs"].get("C5_full")
+        if gold is not None:
+            h = hashlib.sha256()
+            h.update(bins[:m].cpu().numpy().astype("<f8").tobytes())
+            h.update(chi[:m].cpu().numpy().astype("<i8").tobytes())
+            golden_ok = h.hexdigest() == gold["digest"]
     if rank == 0:
         print(json.dumps({"config": f"C5 {S}^3 u8 streamed from pinned host, {world} GPU(s)",
                           "seconds": t, "gvox_s": S ** 3 / t / 1e9,
                           "h2d_gbs_per_gpu": (sh.planes * plane) / t / 1e9, "chi_end_is_1": ok,
+                          "golden_ok": golden_ok,
                           "points": m, "chunk_planes": args.chunk_planes,
                           "backend": args.dist_backend if world > 1 else None}), flush=True)
     if dist is not None:
