@@ -23,6 +23,8 @@ int ecc_oracle_vcec_u8(const uint8_t*, uint64_t, uint64_t, uint64_t, int64_t*, i
 int ecc_oracle_vcec_u16(const uint16_t*, uint64_t, uint64_t, uint64_t, int64_t*, int64_t*);
 int64_t ecc_oracle_vcec_f32(const float*, uint64_t, uint64_t, uint64_t, float*, int64_t*);
 void ecc_oracle_fill_u8(uint8_t*, uint64_t, uint64_t, uint64_t);
+int ecc_oracle_changes_u16_as_f32(const uint16_t*, uint64_t, uint64_t, uint64_t, int8_t*);
+int ecc_oracle_changes_u8(const uint8_t*, uint64_t, uint64_t, uint64_t, int8_t*);
 void ecc_oracle_uniform_noise(float*, uint64_t, uint64_t);
 int ecc_oracle_gaussian_smooth(const float*, float*, uint64_t, uint64_t, uint64_t, double, int);
 }
@@ -359,6 +361,49 @@ TEST_GPU("FileSource: raw f32 little / big endian, NaN and size errors (chunk.hp
   CHECK_THROWS_WITH(process_image(nan, plan), "NaN value at linear index 182");
   std::remove(le.c_str());
   std::remove(be.c_str());
+} END_TEST
+
+TEST_GPU("PaddedChunk API on the device: u16 / u8 chunks, 2D and 3D, faces vs changes") {
+  std::mt19937 rng(123);
+  for (const Dims d : {Dims{7, 9, 11}, Dims{8, 13, 1}, Dims{5, 4, 33}}) {
+    // u16: compute_changes of a middle chunk == the oracle's changes of those rows
+    Image<std::uint16_t> im{d, std::vector<std::uint16_t>(d.voxel_count())};
+    for (auto& v : im.values) v = (std::uint16_t)(rng() % 5 + (rng() % 3) * 40000);
+    std::vector<std::int8_t> want(d.voxel_count());
+    ecc_oracle_changes_u16_as_f32(im.values.data(), d.w0, d.w1, d.w2, want.data());
+    const std::uint64_t b = 2, e = d.w0 - 1, row = d.w1 * d.w2;
+    const auto ch = extract_padded_chunk(im, b, e);
+    std::vector<std::int8_t> got(ch.owned_voxels());
+    compute_changes(ch, 0, ch.owned_len(), got);
+    CHECK(std::equal(got.begin(), got.end(), want.begin() + b * row));
+    // every owned voxel: the signed count of the faces introduced() reports
+    // (each face's dimension d - nnz) equals voxel_contribution()
+    const int dd = d.is_2d() ? 2 : 3;
+    for (std::uint64_t i = b; i < e; i += 2)
+      for (std::uint64_t j = 0; j < d.w1; j += 3)
+        for (std::uint64_t k = 0; k < d.w2; k += 5) {
+          int sum = dd == 2 ? 1 : -1;
+          for (int a0 = -1; a0 <= 1; ++a0)
+            for (int a1 = -1; a1 <= 1; ++a1)
+              for (int a2 = (dd == 2 ? 0 : -1); a2 <= (dd == 2 ? 0 : 1); ++a2) {
+                if (!a0 && !a1 && !a2) continue;
+                if (introduced(ch, {i, j, k}, {a0, a1, a2}))
+                  sum += ((dd - (a0 != 0) - (a1 != 0) - (a2 != 0)) % 2 == 0) ? 1 : -1;
+              }
+          CHECK(sum == voxel_contribution(ch, {i, j, k}));
+          CHECK(sum == want[(i * d.w1 + j) * d.w2 + k]);
+        }
+    // u8: accumulate_dense_u8 over row pieces == the per-value sums of the changes
+    Image<std::uint8_t> i8{d, std::vector<std::uint8_t>(d.voxel_count())};
+    for (auto& v : i8.values) v = (std::uint8_t)(rng() % 6);
+    std::vector<std::int8_t> w8(d.voxel_count());
+    ecc_oracle_changes_u8(i8.values.data(), d.w0, d.w1, d.w2, w8.data());
+    const auto c8 = extract_padded_chunk(i8, 0, d.w0);
+    std::vector<std::int64_t> acc(256, 0), ref(256, 0);
+    for (std::uint64_t r = 0; r < d.w0; ++r) accumulate_dense_u8<std::int64_t>(c8, r, r + 1, acc);
+    for (std::uint64_t v = 0; v < d.voxel_count(); ++v) ref[i8.values[v]] += w8[v];
+    CHECK(acc == ref);
+  }
 } END_TEST
 
 TEST_GPU("device curve text == write_curve (curve.hpp:87-121), f32 thresholds") {
