@@ -102,12 +102,12 @@ __global__ void __launch_bounds__(NT, 1)
           // the packed table of hist16.cuh: exact out-of-band moves to the
           // per-SM scratch row
           hist16::Upd u;
-          hist16::issue(hbase, v, (uint32_t)ch, u);  // 32-bit two's complement (no borrow: biased)
+          hist16::issue(hbase, v, (uint32_t)ch, u);  // 32-bit two's complement
           auto spill = [&](uint32_t key, int val) {
             atomicAdd(&scratch[key], val);
             atomicOr(&spilled[key >> 5], 1u << (key & 31));
           };
-          hist16::fix(hbase, u, hist16::crossed(u), spill);
+          hist16::fix(hbase, u, spill);
         } else {
           atomicAdd(&bins[v], (uint32_t)ch);
         }
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t b0 = min(nbins, threadIdx.x * per), b1 = min(nbins, b0 + per);
   auto bin_sum = [&](uint32_t b) -> int {
     if constexpr (PACKED) {
-      int s = (int)((bins[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
+      int s = hist16::half_value(bins[b >> 1], b & 1u);
       if ((spilled[b >> 5] >> (b & 31)) & 1u) s += scratch[b];
       return s;
     } else {

@@ -41,7 +41,6 @@ constexpr int HGRP = ECC_HGRP;  // pixels per atomic group (divides 32)
 #define ECC_B16_ASYNC 1
 #endif
 static_assert(hist16::no_wrap(NT, HGRP, 3), "2D changes reach -3: the packed halves could wrap");
-constexpr uint32_t BIAS = 0x80008000u;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -84,7 +83,7 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* hw = sm;                    // packed halves
   uint32_t* pres = hw + HWORDS;         // occupancy bits
   uint32_t* spilled = pres + PWORDS;    // bins with a spilled partial in `scratch`
-  for (int i = threadIdx.x; i < HWORDS; i += NT) hw[i] = BIAS;
+  for (int i = threadIdx.x; i < HWORDS; i += NT) hw[i] = hist16::BIAS;
   for (int i = threadIdx.x; i < 2 * PWORDS; i += NT) pres[i] = 0;
   __syncthreads();
   const uint16_t* img = data + (size_t)blockIdx.x * h * w;
@@ -262,12 +261,12 @@ __global__ void __launch_bounds__(NT, 1)
             hist16::mark(pbase, key, (vmr >> p) & 1u);
             hist16::issue(hbase, key, chu, u[j]);
           }
-          uint32_t cr[HGRP], any = 0;
+          uint32_t any = 0;
 #pragma unroll
-          for (int j = 0; j < HGRP; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          for (int j = 0; j < HGRP; ++j) any |= hist16::crossed(u[j]);
           if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-            for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, u[j], cr[j], spill);
+            for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, u[j], spill);
           }
         }
       }
@@ -294,10 +293,10 @@ __global__ void __launch_bounds__(NT, 1)
   int32_t* row = chi + (size_t)blockIdx.x * 65536;
   auto sums4 = [&](uint32_t b, int (&x)[4]) {  // b % 4 == 0
     const uint2 w2 = *reinterpret_cast<const uint2*>(hw + (b >> 1));
-    x[0] = (int)(w2.x & 0xFFFFu) - 32768;
-    x[1] = (int)(w2.x >> 16) - 32768;
-    x[2] = (int)(w2.y & 0xFFFFu) - 32768;
-    x[3] = (int)(w2.y >> 16) - 32768;
+    x[0] = hist16::lo_value(w2.x);
+    x[1] = hist16::hi_value(w2.x);
+    x[2] = hist16::lo_value(w2.y);
+    x[3] = hist16::hi_value(w2.y);
     const uint32_t sp = (spilled[b >> 5] >> (b & 31)) & 0xFu;
     if (sp) {
 #pragma unroll

@@ -200,12 +200,12 @@ __global__ void __launch_bounds__(NT, 1)
               hist16::mark(pbase, key, (vmr >> p) & 1u);
               hist16::issue(hbase, key, chu, up[j]);
             }
-            uint32_t cr[HGRP], any = 0;
+            uint32_t any = 0;
 #pragma unroll
-            for (int j = 0; j < HGRP; ++j) any |= (cr[j] = hist16::crossed(up[j]));
+            for (int j = 0; j < HGRP; ++j) any |= hist16::crossed(up[j]);
             if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-              for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, up[j], cr[j], spill);
+              for (int j = 0; j < HGRP; ++j) hist16::fix(hbase, up[j], spill);
             }
           }
         }
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < g.nbins; b += NT) {
-    const int sum = (int)((hw[b >> 1] >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
+    const int sum = hist16::half_value(hw[b >> 1], b & 1u);
     if (sum != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[b]),
                 static_cast<unsigned long long>(static_cast<long long>(sum)));

@@ -19,7 +19,7 @@
 //    complement, and replicating the sign plane makes the code transpose
 //    produce signed bytes that one PRMT sign-extends.
 //  * Histogram: 65536 signed 16-bit halves packed two per word in shared
-//    memory, each biased by 32768 (hist16.cuh): an update that leaves its
+//    memory, stored as v + 0x1000 (hist16.cuh): an update that leaves its
 //    half outside [-4096, 4095] moves the half's current value to the global
 //    int64 histogram with a compare-and-swap, so the half is reset to exactly
 //    0; the group size keeps the worst-case drift before the first reset
@@ -50,7 +50,6 @@ constexpr int RING_BYTES = NW * NS * STAGE;
 constexpr int BAR_BYTES = NW * NS * 8;
 constexpr int SMEM_BYTES = RING_BYTES + BAR_BYTES + (HWORDS + PWORDS + 1) * 4;  // + set-bit count
 constexpr uint32_t FULL = 0xFFFFFFFFu;
-constexpr uint32_t BIAS = 0x80008000u;  // both halves at 32768
 #ifndef ECC_AFF_U
 #define ECC_AFF_U 8
 #endif
@@ -337,12 +336,12 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
             }
             hist16::issue(hbase, key, chu, u[j]);
           }
-          uint32_t cr[GRP], any = 0;
+          uint32_t any = 0;
 #pragma unroll
-          for (int j = 0; j < GRP; ++j) any |= (cr[j] = hist16::crossed(u[j]));
+          for (int j = 0; j < GRP; ++j) any |= hist16::crossed(u[j]);
           if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-            for (int j = 0; j < GRP; ++j) hist16::fix(hbase, u[j], cr[j], spill);
+            for (int j = 0; j < GRP; ++j) hist16::fix(hbase, u[j], spill);
           }
         }
       };
@@ -369,7 +368,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t(*myring)[STAGE] = ring[warp];
   uint64_t* myfull = full[warp];
-  for (int i = threadIdx.x; i < HWORDS; i += NW * 32) hwords[i] = BIAS;
+  for (int i = threadIdx.x; i < HWORDS; i += NW * 32) hwords[i] = hist16::BIAS;
   for (int i = threadIdx.x; i <= PWORDS; i += NW * 32) pres[i] = 0;  // bitmap + count
   if (lane == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&myfull[s], 1);
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < g.nbins; b += NW * 32) {
     const uint32_t word = hwords[b >> 1];
-    const int sum = (int)((word >> ((b & 1) << 4)) & 0xFFFFu) - 32768;
+    const int sum = hist16::half_value(word, b & 1u);
     if (sum != 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[b]),
                 static_cast<unsigned long long>(static_cast<long long>(sum)));

@@ -3,12 +3,14 @@
 // Built and run by tests/test_native_cpu.py.
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <random>
 
 #define __host__
 #define __device__
 #define __forceinline__ inline
 #include "../../paper_2203_09087_b200/csrc/bits.cuh"
+#include "../../paper_2203_09087_b200/csrc/hist16.cuh"
 
 int main() {
   std::mt19937 rng(7);
@@ -53,7 +55,7 @@ int test_transpose_codes() {
   std::printf("transpose_codes ok\n");
   return 0;
 }
-static int run_extra = [] { return test_transpose_codes(); }();
+static int run_extra = [] { if (test_transpose_codes()) std::exit(1); return 0; }();  // a failure fails the binary
 // (appended) sum_blocks9: every one of the 3^9 per-block (h, l) patterns
 int test_sum_blocks9() {
   int pat = 0;
@@ -83,4 +85,34 @@ int test_sum_blocks9() {
   std::printf("sum_blocks9 ok (%d patterns)\n", pat);
   return 0;
 }
-static int run_extra9 = [] { return test_sum_blocks9(); }();
+static int run_extra9 = [] { if (test_sum_blocks9()) std::exit(1); return 0; }();  // a failure fails the binary
+
+// hist16.cuh's packed encoding: every pair of half sums |v| < 32768 decodes
+// exactly from the word  BIAS + v_lo + (v_hi << 16)  (plain 32-bit adds, the
+// low half borrowing from the high one), and the one-mask band flag fires for
+// every half outside the band widened by one count (the borrow's lag).
+static int test_hist16() {
+  using namespace eccb::hist16;
+  std::mt19937 rng(11);
+  const int edges[] = {-32767, -28672, -4098, -4097, -4096, -4095, -1, 0, 1, 4094, 4095, 4096, 4097, 28671, 32767};
+  long n = 0;
+  for (int vlo = -32767; vlo <= 32767; ++vlo) {
+    for (int k = 0; k < 15 + 8; ++k) {
+      const int vhi = k < 15 ? edges[k] : (int)(rng() % 65535) - 32767;
+      const uint32_t w = BIAS + (uint32_t)vlo + ((uint32_t)vhi << 16);
+      if (lo_value(w) != vlo || hi_value(w) != vhi || half_value(w, 0) != vlo || half_value(w, 1) != vhi) {
+        std::printf("hist16 decode mismatch %d %d\n", vlo, vhi);
+        return 1;
+      }
+      const bool flo = (w & FLAG & 0xFFFFu) != 0, fhi = (w & FLAG & 0xFFFF0000u) != 0;
+      const bool olo = vlo < -BAND || vlo >= BAND;
+      if (flo != olo) { std::printf("hist16 low flag %d\n", vlo); return 1; }
+      if ((vhi < -BAND - 1 || vhi > BAND) && !fhi) { std::printf("hist16 high flag missed %d %d\n", vlo, vhi); return 1; }
+      if (vlo >= -BAND && (vhi < -BAND || vhi >= BAND) != fhi) { std::printf("hist16 high flag %d %d\n", vlo, vhi); return 1; }
+      ++n;
+    }
+  }
+  std::printf("hist16 encoding ok (%ld words)\n", n);
+  return 0;
+}
+static int run_hist16 = [] { if (test_hist16()) std::exit(1); return 0; }();  // a failure fails the binary

@@ -25,7 +25,8 @@ def _run(args, timeout=600):
 
 def test_bit_sliced_sum_and_code_transpose():
     out = _run([_bin("test_bits")])
-    assert "sum_code ok" in out and "transpose_codes ok" in out
+    for name in ("sum_code", "transpose_codes", "sum_blocks9", "hist16 encoding"):
+        assert f"{name} ok" in out, out
 
 
 def test_cpp_api_host_cases():
