@@ -71,6 +71,16 @@ __host__ __device__ __forceinline__ uint32_t shr_fma(uint32_t x, int k) {
 #endif
 }
 
+// (x >> p) & 1 for a compile-time p on the FMA pipe: IMAD.SHL moves bit p
+// to bit 31, IMAD.HI by 2 brings it down alone.
+__host__ __device__ __forceinline__ uint32_t bit_fma(uint32_t x, int p) {
+#ifdef __CUDA_ARCH__
+  return __umulhi(x << (31 - p), 2u);
+#else
+  return (x >> p) & 1u;
+#endif
+}
+
 // Merge-style delta swap between w[i] and w[i+s] on bit distance `sh` with
 // mask m (bits that stay in w[i]): one shift + one lop3 per output word
 // (the left shift becomes IMAD.SHL, the right one IMAD.HI: both FMA pipe).

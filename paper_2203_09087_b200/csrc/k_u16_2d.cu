@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(NT, 1)
               const uint32_t chu =
                   bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
               const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
-              hist16::mark(pbase, key, (vmr >> p) & 1u);
+              hist16::mark(pbase, key, bits::bit_fma(vmr, p));  // (vmr >> p) & 1 on the FMA pipe
               hist16::issue(hbase, key, chu, up[j]);
             }
             uint32_t any = 0;
