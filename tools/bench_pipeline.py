@@ -1,7 +1,7 @@
 """bench_run (pipeline.hpp:236-291) on the GPU beside the reference's own
 bench_run on the host cores, same dims / iterations / sigma / width.
 
-  python tools/bench_pipeline.py [side] [iterations] [ref_side]
+  python tools/bench_pipeline.py [side] [iterations] [ref_side]   (ref_side 0: GPU only)
 """
 import json
 import os
@@ -21,7 +21,7 @@ ctx.bench_run(eb.Dims(side, side, side), 1)  # warm-up at the same size (allocat
 rep = ctx.bench_run(eb.Dims(side, side, side), iters)
 out = {"impl": "b200", "dims": [side] * 3, **rep.__dict__}
 print(json.dumps(out), flush=True)
-if oracle.ref_available():
+if ref_side > 0 and oracle.ref_available():
     r = oracle.ref_bench_run((ref_side,) * 3, 1)
     print(json.dumps({"impl": "reference (host cores)", "dims": [ref_side] * 3, "iterations": 1, **r}),
           flush=True)
