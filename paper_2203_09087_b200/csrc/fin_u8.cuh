@@ -8,6 +8,7 @@
 #pragma once
 #include <cstdint>
 
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 namespace eccb {
@@ -181,6 +182,69 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
     *fin.count = (uint64_t)total.x;
     *fin.ticket = 0;
   }
+}
+
+// Small images in ONE thread-block cluster (k_u8_2d's cluster path, one
+// GPU): every CTA reduces its table to per-value (sum, count) and stores
+// them straight into CTA 0's shared memory (distributed shared memory,
+// fire-and-forget stores); after one cluster barrier CTA 0 sums the rows
+// and writes the curve -- no global histogram, no atomics, no ticket, no
+// L2 round trip.  `fin.ticket` and the global histogram stay untouched (zero).
+constexpr int kMaxCluster = 16;
+// rows: kMaxCluster x 256 sums then kMaxCluster x 256 counts (dynamic shared
+// memory, cluster_rows_bytes).
+constexpr int cluster_rows_bytes = 2 * kMaxCluster * 256 * 4;
+template <int NT, class Code, int REP = 1>
+__device__ __forceinline__ void cluster_finalize(const uint32_t* hist, int* rows, const Fin& fin) {
+  static_assert(NT >= 256, "one thread per value");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  // rows [rank][value] of CTA 0's copy; int32: a cluster holds < 2^31 / 7 pixels
+  int(*rows_s)[256] = reinterpret_cast<int(*)[256]>(rows);
+  int(*rows_c)[256] = reinterpret_cast<int(*)[256]>(rows + kMaxCluster * 256);
+  const unsigned rank = cluster.block_rank(), nb = cluster.num_blocks();
+  __syncthreads();
+  for (int v = threadIdx.x; v < 256; v += NT) {
+    int sum = 0, cnt = 0;
+#pragma unroll
+    for (int c = 0; c < Code::n; ++c) {
+      if (!Code::live(c)) continue;
+      int n = 0;
+#pragma unroll
+      for (int r = 0; r < REP; ++r) n += (int)hist[(c * 256 + v) * REP + r];
+      cnt += n;
+      sum += n * Code::change(c);
+    }
+    *cluster.map_shared_rank(&rows_s[rank][v], 0) = sum;
+    *cluster.map_shared_rank(&rows_c[rank][v], 0) = cnt;
+  }
+  cluster.sync();  // release / acquire: every CTA's row is in CTA 0
+  if (rank != 0) return;
+  struct Add {
+    __device__ longlong2 operator()(const longlong2& a, const longlong2& b) const {
+      return make_longlong2(a.x + b.x, a.y + b.y);
+    }
+  };
+  using Scan = cub::BlockScan<longlong2, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int v = threadIdx.x;
+  long long s = 0, n = 0;
+  if (v < 256) {
+#pragma unroll
+    for (int r = 0; r < kMaxCluster; ++r)
+      if (r < (int)nb) {
+        s += rows_s[r][v];
+        n += rows_c[r][v];
+      }
+  }
+  longlong2 ex, total;
+  Scan(tmp).ExclusiveScan(make_longlong2(n != 0, s), ex, make_longlong2(0, 0), Add(), total);
+  if (n != 0) {
+    fin.bins[ex.x] = v;
+    fin.changes[ex.x] = s;
+    fin.chi[ex.x] = ex.y + s;
+  }
+  if (threadIdx.x == 0) *fin.count = (uint64_t)total.x;
 }
 
 }  // namespace u8fin

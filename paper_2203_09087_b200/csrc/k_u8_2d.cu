@@ -103,6 +103,7 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return v;
 }
 
+template <bool CLUSTER>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_u8_2d(const Geom g, int64_t* __restrict__ ghist, const u8fin::Fin fin) {
   __shared__ __align__(16) uint32_t hist[HIST_WORDS];
@@ -225,7 +226,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
   }
-  u8fin::flush_and_finalize<NT, Codes, HREP>(hist, ghist, fin);
+  if constexpr (CLUSTER) {
+    extern __shared__ __align__(16) int cluster_rows[];
+    u8fin::cluster_finalize<NT, Codes, HREP>(hist, cluster_rows, fin);
+  } else {
+    u8fin::flush_and_finalize<NT, Codes, HREP>(hist, ghist, fin);
+  }
 }
 
 }  // namespace u82d
@@ -251,6 +257,58 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   g.nchunks = (g.W1 + 31) / 32;
   g.nstrips = (g.nchunks + STRIP - 1) / STRIP;
   g.four = 4 * HREP;
+  u8fin::Fin fin{};
+  if (fz) {
+    fin = u8fin::Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
+    fin.x = u8fin::Xchg{fz->world, fz->rank, fz->epoch, fz->slots, fz->flags, fz->my_slots,
+                        fz->my_flags, fz->err};
+  }
+  // Small images with the fused curve on one GPU (C1): all CTAs in one
+  // thread-block cluster, the curve reduced over distributed shared memory
+  // (fin_u8.cuh, cluster_finalize) -- bands of up to 4 rows so the units fit
+  // one cluster of the largest size this kernel can be co-scheduled with.
+  static int max_cluster = -1;  // same on every B200
+  if (max_cluster < 0) {
+    max_cluster = 0;
+    if (cudaFuncSetAttribute(k_u8_2d<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
+            cudaSuccess &&
+        cudaFuncSetAttribute(k_u8_2d<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             u8fin::cluster_rows_bytes) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(u8fin::kMaxCluster);
+      q.blockDim = dim3(NT);
+      q.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+      int cs = 0;
+      if (cudaOccupancyMaxPotentialClusterSize(&cs, k_u8_2d<true>, &q) == cudaSuccess)
+        max_cluster = std::min(cs, u8fin::kMaxCluster);
+    }
+    (void)cudaGetLastError();
+  }
+  if (fz && fz->world <= 1 && max_cluster >= 2 && g.P > 0 && (long long)g.P * g.W1 <= (1ll << 22)) {
+    const long long cap_units = (long long)max_cluster * NW;
+    if (g.nstrips <= cap_units) {
+      const long long per = cap_units / g.nstrips;  // bands that fit the cluster
+      const long long band = (g.P + per - 1) / per;
+      if (band <= 4) {
+        g.band = (int)band;
+        g.nunits = (int)((g.P + band - 1) / band * g.nstrips);
+        const unsigned grid = (unsigned)((g.nunits + NW - 1) / NW);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = grid;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        return cudaLaunchKernelEx(&cfg, k_u8_2d<true>, g, ghist, fin);
+      }
+    }
+  }
   const long long cap_warps = (long long)sms * CTAS_PER_SM * NW;
   // bands of >= 32 rows (2 halo rows per band); ~4 units per resident warp
   // when the image is large enough, else one wave of shorter bands (>= MINBAND:
@@ -265,13 +323,7 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   if (g.P <= 0 || units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
   const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
-  u8fin::Fin fin{};
-  if (fz) {
-    fin = u8fin::Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
-    fin.x = u8fin::Xchg{fz->world, fz->rank, fz->epoch, fz->slots, fz->flags, fz->my_slots,
-                        fz->my_flags, fz->err};
-  }
-  k_u8_2d<<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
+  k_u8_2d<false><<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
   return cudaGetLastError();
 }
 

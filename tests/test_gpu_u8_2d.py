@@ -123,3 +123,32 @@ def test_paper_size_images(ctx, shape):
     b, ch, chi = _device_curve(ctx, dev)
     assert np.array_equal(b, v.astype(np.int32)) and np.array_equal(ch, c)
     assert int(chi[-1]) == 1
+
+
+def test_cluster_path_interleaved_with_large_images(ctx):
+    """Small images run in one thread-block cluster whose CTA 0 reduces the
+    histogram over distributed shared memory (fin_u8.cuh, cluster_finalize)
+    and never touches the fused global histogram or ticket; larger images use
+    the global-atomics path.  Alternate the two (bands of 1..4 rows and the
+    band-5 boundary at 1025 x 256) and check every curve."""
+    rng = np.random.default_rng(23)
+    shapes = [(256, 256), (1500, 1500), (512, 512), (1024, 256), (1025, 256), (3, 1000),
+              (2048, 300), (300, 1000), (1, 5000), (767, 511)]
+    for shape in shapes + shapes[::-1]:
+        img = rng.integers(0, 256, shape).astype(np.uint8)
+        _check(ctx, img)
+        # the device-resident single-launch curve as well
+        import torch
+        d = torch.from_numpy(img).cuda()
+        bins = torch.empty(256, dtype=torch.int32, device="cuda")
+        chg = torch.empty(256, dtype=torch.int64, device="cuda")
+        chi = torch.empty(256, dtype=torch.int64, device="cuda")
+        cnt = torch.empty(1, dtype=torch.int64, device="cuda")
+        ctx.curve_device(d, eb.Dims(shape[0], shape[1], 1), bins, chg, chi, cnt)
+        torch.cuda.synchronize()
+        v, c = oracle.vcec(img)
+        m = int(cnt.item())
+        assert m == len(v), shape
+        assert np.array_equal(bins[:m].cpu().numpy().astype(np.int64), v.astype(np.int64)), shape
+        assert np.array_equal(chg[:m].cpu().numpy(), c), shape
+        assert np.array_equal(chi[:m].cpu().numpy(), np.cumsum(c)), shape
