@@ -191,6 +191,11 @@ __device__ __forceinline__ void flush_and_finalize(const uint32_t* hist, int64_t
 // and writes the curve -- no global histogram, no atomics, no ticket, no
 // L2 round trip.  `fin.ticket` and the global histogram stay untouched (zero).
 constexpr int kMaxCluster = 16;
+// first half of the "every CTA of the cluster has started" barrier; called
+// by every thread at the kernel's start, completed in cluster_finalize
+__device__ __forceinline__ void cluster_started_arrive() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 // rows: kMaxCluster x 256 sums then kMaxCluster x 256 counts (dynamic shared
 // memory, cluster_rows_bytes).
 constexpr int cluster_rows_bytes = 2 * kMaxCluster * 256 * 4;
@@ -204,6 +209,10 @@ __device__ __forceinline__ void cluster_finalize(const uint32_t* hist, int* rows
   int(*rows_c)[256] = reinterpret_cast<int(*)[256]>(rows + kMaxCluster * 256);
   const unsigned rank = cluster.block_rank(), nb = cluster.num_blocks();
   __syncthreads();
+  // CTA 0 must have started before its shared memory is written remotely:
+  // the kernel arrived on the cluster barrier at its start
+  // (cluster_started_arrive); this wait completes that phase
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   for (int v = threadIdx.x; v < 256; v += NT) {
     int sum = 0, cnt = 0;
 #pragma unroll

@@ -106,6 +106,7 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 template <bool CLUSTER>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_u8_2d(const Geom g, int64_t* __restrict__ ghist, const u8fin::Fin fin) {
+  if constexpr (CLUSTER) u8fin::cluster_started_arrive();
   __shared__ __align__(16) uint32_t hist[HIST_WORDS];
   for (int i = threadIdx.x; i < HIST_WORDS; i += NT) hist[i] = 0;
   __syncthreads();
@@ -290,9 +291,10 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
       const long long per = cap_units / g.nstrips;  // bands that fit the cluster
       const long long band = (g.P + per - 1) / per;
       if (band <= 4) {
-        g.band = (int)band;
-        g.nunits = (int)((g.P + band - 1) / band * g.nstrips);
-        const unsigned grid = (unsigned)((g.nunits + NW - 1) / NW);
+        Geom gc = g;
+        gc.band = (int)band;
+        gc.nunits = (int)((g.P + band - 1) / band * g.nstrips);
+        const unsigned grid = (unsigned)((gc.nunits + NW - 1) / NW);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(NT);
@@ -305,7 +307,10 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        return cudaLaunchKernelEx(&cfg, k_u8_2d<true>, g, ghist, fin);
+        if (cudaLaunchKernelEx(&cfg, k_u8_2d<true>, gc, ghist, fin) == cudaSuccess) return cudaSuccess;
+        // the cluster could not be placed (e.g. SMs held by other work): the
+        // regular launch below computes the same curve
+        (void)cudaGetLastError();
       }
     }
   }
