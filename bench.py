@@ -570,6 +570,10 @@ def main():
     # K steps enqueued back to back (the host runs ahead, so launch latency is
     # hidden behind the previous step's L2 flush); each step is bracketed by
     # CUDA events on the compute stream, the whole region by barrier + sync.
+    # A fused step is ONE kernel launch, so its bracket is the kernel's time
+    # too; the NCCL fallback step (accumulate, all-reduce, finalize) also
+    # brackets its accumulate kernel for the roofline.
+    single_launch = xchg is not None or dist is None
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     R.barrier()
     torch.cuda.synchronize()
@@ -579,7 +583,10 @@ def main():
             with torch.cuda.stream(stream):
                 flush.fill_(1)  # evict L2 (126 MB) between timed steps
             a.record(stream)
-            step(k0, k1)
+            if single_launch:
+                step()
+            else:
+                step(k0, k1)
             b.record(stream)
         torch.cuda.synchronize()
         R.barrier()
@@ -591,7 +598,7 @@ def main():
     ok1, g1 = check_curve(bins, chi, cnt, 256, 1.0, gold_c2)
     assert R.all_true(ok1 and g1 is not False), "curve check failed after the timed steps"
     step_ms = [a.elapsed_time(b) for a, b, _, _ in evs]
-    kern_ms = [k0.elapsed_time(k1) for _, _, k0, k1 in evs]
+    kern_ms = step_ms if single_launch else [k0.elapsed_time(k1) for _, _, k0, k1 in evs]
     t_step = sum(step_ms) / len(step_ms)
     t_kern = sum(kern_ms) / len(kern_ms)
     t_step, t_kern = R.max(t_step, t_kern)
