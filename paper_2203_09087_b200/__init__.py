@@ -479,13 +479,26 @@ class Context:
         cap = 256 if dt == ECC_U8 else (65536 if dt == ECC_U16 else dims.voxel_count())
         if dt == ECC_F32 and bm.kind == ECC_BIN_AFFINE:
             cap = bm.nbins
-        vals = np.empty(cap, _NP[dt])
-        series = np.empty(cap, np.int64)
-        n = _u64()
-        _check(fn(self._p, data, where, dt, _Dims(dims.w0, dims.w1, dims.w2), C.byref(bm),
-                  vals.ctypes.data, series.ctypes.data, cap, C.byref(n)))
-        m = n.value
-        return vals[:m].copy(), series[:m].copy()
+        elif dt == ECC_F32:
+            # distinct f32 values: rarely near one per voxel, so start at 4 M
+            # points (48 MB) and call again at the exact size if they are more
+            cap = min(cap, 1 << 22)
+
+        def run(cap):
+            vals = np.empty(cap, _NP[dt])
+            series = np.empty(cap, np.int64)
+            n = _u64()
+            rc = fn(self._p, data, where, dt, _Dims(dims.w0, dims.w1, dims.w2), C.byref(bm),
+                    vals.ctypes.data, series.ctypes.data, cap, C.byref(n))
+            return rc, vals, series, n.value
+
+        rc, vals, series, m = run(cap)
+        if rc == ECC_EINVAL and m > cap:  # "output capacity ... is below the m values"
+            rc, vals, series, m = run(m)
+        _check(rc)
+        if 2 * m < cap:  # small result: do not keep the oversized arrays alive
+            return vals[:m].copy(), series[:m].copy()
+        return vals[:m], series[:m]
 
     def vcec(self, image, binmap=None) -> GlobalVcec:
         v, c = self._volume(lib().ecc_vcec, image, binmap)

@@ -124,6 +124,37 @@ struct PinBuf {
 
 }  // namespace
 
+// Host vectors of a result: no value-initialisation on resize (every
+// element is then written by a device copy), kept in the context between
+// calls so a large result reuses already-touched pages.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = NoInitAlloc<U>;
+  };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using HostVec = std::vector<T, NoInitAlloc<T>>;
+
+struct BinResult {
+  HostVec<uint32_t> bins;     // identity / affine
+  HostVec<uint32_t> keys;     // sorted path (order keys)
+  HostVec<int64_t> changes;
+  HostVec<int64_t> chi;
+};
+
 struct ecc_ctx {
   int device = 0;
   int sms = 148;
@@ -146,6 +177,7 @@ struct ecc_ctx {
   DevBuf nanidx;    // per-chunk first NaN index of the file path
   DevBuf bscratch;  // per-SM int32[65536] spill rows of the u16 batched kernel (kept zero)
   cudaEvent_t ov_ev[17] = {};  // overlapped host-input path: start + one per chunk copy
+  BinResult hres;  // host side of the last host-returning call (pages reused)
 };
 
 // Multi-GPU rank exchange over peer memory (fin_u8.cuh, Xchg): this rank's
@@ -394,13 +426,6 @@ int accumulate(ecc_ctx* ctx, const Slab& s0, ecc_dtype dtype, bool affine,
 }
 
 // Result of a whole-volume or streamed run, in bin space.
-struct BinResult {
-  std::vector<uint32_t> bins;     // identity / affine
-  std::vector<uint32_t> keys;     // sorted path (order keys)
-  std::vector<int64_t> changes;
-  std::vector<int64_t> chi;
-};
-
 // Whole 3D u8 image in ONE launch (k_u8_3d with the fused last-CTA K3).
 bool fusable(ecc_dtype dtype, const Slab& s, bool affine) {
   return dtype == ECC_U8 && !affine && (u8_3d_supported(s) || u8_2d_supported(s));
@@ -1217,7 +1242,7 @@ static int volume_common(ecc_ctx* ctx, const void* data, int where, ecc_dtype dt
   // them into the result block): clear what an earlier rejected call left
   CKI(ctx->flags.ensure(16));
   CKR(cudaMemsetAsync(ctx->flags.p, 0, 4, st));
-  BinResult r;
+  BinResult& r = ctx->hres;
   bool sorted = false;
   AffineMap am{};
   bool done = false;
@@ -1400,7 +1425,7 @@ static int stream_impl(ecc_ctx* ctx, ecc_read_rows_fn read_rows, void* user,
         return fail(ECC_ESOURCE, "ingestion of chunk " + std::to_string(k) +
                                      " failed: NaN value at linear index " + std::to_string(nan[k]));
   }
-  BinResult r;
+  BinResult& r = ctx->hres;
   if (sorted) {
     CKI(read_flags(ctx, st));
     CKI(sorted_finish(ctx, st, sorted_n, nchunks > 1, &r));
@@ -1614,7 +1639,7 @@ int ecc_process_host(ecc_ctx* ctx, const void* host, ecc_dtype dtype, ecc_dims d
   CKI(host_pipeline(ctx, host, 0, dims.w0, dtype, dims, bounds, nchunks, affine, am, nbins,
                     ctx->hist.as<int64_t>(), timings));
   if (affine) CKI(read_flags(ctx, st));
-  BinResult r;
+  BinResult& r = ctx->hres;
   CKI(finalize_to_host(ctx, (uint32_t)nbins, st, &r));
   const size_t m = r.changes.size();
   *n_out = m;

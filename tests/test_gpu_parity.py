@@ -581,3 +581,18 @@ def test_overlapped_host_input_dense_maps(ctx, case):
         bad[40, 7, 9] = 0.3
         with pytest.raises(eb.EccError):
             ctx.vcec(bad, binmap=bm)
+
+
+def test_f32_more_distinct_values_than_the_first_capacity(ctx):
+    """The Python wrapper first asks for 4 M points; a volume with more
+    distinct f32 values (almost one per voxel here) gets the exact count back
+    and is called again at that size (ecc_vcec reports the count with the
+    capacity error).  Both the VCEC and the curve stay bit-exact."""
+    rng = np.random.default_rng(41)
+    img = rng.standard_normal((264, 128, 128), dtype=np.float32)  # ~all distinct
+    got = ctx.vcec(img)
+    v, c = oracle.vcec(img)
+    assert got.size() > (1 << 22)
+    assert np.array_equal(np.asarray(got.values), v) and np.array_equal(np.asarray(got.changes), c)
+    cur = ctx.curve(img)
+    assert np.array_equal(np.asarray(cur.chi), np.cumsum(c))
