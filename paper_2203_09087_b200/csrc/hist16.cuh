@@ -40,7 +40,7 @@
 // GROUP x MAX|change| past the widened band edge, which must stay below
 // HEADROOM = 32768 - BAND - 1 to keep |v| < 32768:
 //   k_u16_3d   384 threads x 10 voxels x 7 = 26880 < 28671
-//   k_u16_2d   512 x 8 x 3 = 12288;  k_batch16  512 x 8 x 3 = 12288;
+//   k_u16_2d   512 x 8 x 3 = 12288;  k_batch16  512 x 16 x 3 = 24576;
 //   k_batch (wide u16 batched)  1024 x 1 x 3 = 3072.
 #pragma once
 #include <cstdint>
