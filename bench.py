@@ -491,37 +491,54 @@ def main():
     xchg = None
     exchange = "none" if dist is None else f"{R.backend}_allreduce"
     if dist is not None and not args.no_p2p:
+        # every collective below is reached by every rank whatever fails
+        # locally, so a rank whose peer mappings fail cannot strand the others
+        x, why = None, ""
         try:
             x = eb.Exchange(ctx, rank, world)
-            handles = [None] * world
-            dist.all_gather_object(handles, x.handle)
-            x.open(handles)
+            h = x.handle
+        except Exception as e:
+            h, why = None, str(e)[:80]
+        handles = [None] * world
+        dist.all_gather_object(handles, h)
+        ok = all(hh is not None for hh in handles)  # the same on every rank
+        if ok:
+            try:
+                x.open(handles)
+            except Exception as e:
+                ok, why = False, str(e)[:80]
+            ok = R.all_true(ok)
+        if ok:
             ref = []
-            for use in (None, x):  # one all-reduce step, one fused step: same curve?
-                with torch.cuda.stream(stream):
-                    if use is None:
-                        hist.zero_()
-                        sharded_histogram(sh, lambda shd, h: ctx.accumulate_slab(
-                            slab, dims, shd.plane0, shd.own0, shd.own1, h, stream=ctx.stream),
-                            hist, dist.all_reduce)
-                        ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
-                    else:
-                        ctx.curve_sharded(x, slab, dims, p0, own0, own1, bins, chg, chi, cnt,
-                                          stream=ctx.stream)
-                torch.cuda.synchronize()
-                if use is not None:
-                    x.status()
-                ref.append((cnt.clone(), chi.clone(), bins.clone()))
-            same = all(torch.equal(a, b) for a, b in zip(ref[0], ref[1]))
-            if R.all_true(same):
-                xchg, exchange = x, "p2p_fused_exchange"
-            else:
-                x.close()
-        except Exception as e:  # fall back to the all-reduce, reported in the JSON
-            exchange = f"{R.backend}_allreduce (p2p setup failed: {str(e)[:80]})"
-        if not R.all_true(xchg is not None) and xchg is not None:  # every rank must agree
-            xchg.close()
-            xchg, exchange = None, f"{R.backend}_allreduce"
+            try:
+                for use in (None, x):  # one all-reduce step, one fused step: same curve?
+                    with torch.cuda.stream(stream):
+                        if use is None:
+                            hist.zero_()
+                            sharded_histogram(sh, lambda shd, h: ctx.accumulate_slab(
+                                slab, dims, shd.plane0, shd.own0, shd.own1, h, stream=ctx.stream),
+                                hist, dist.all_reduce)
+                            ctx.finalize(hist, 256, bins, chg, chi, cnt, stream=ctx.stream)
+                        else:
+                            ctx.curve_sharded(x, slab, dims, p0, own0, own1, bins, chg, chi, cnt,
+                                              stream=ctx.stream)
+                    torch.cuda.synchronize()
+                    if use is not None:
+                        x.status()
+                    ref.append((cnt.clone(), chi.clone(), bins.clone()))
+                same = all(torch.equal(a, b) for a, b in zip(ref[0], ref[1]))
+            except Exception as e:  # fall back to the all-reduce, reported in the JSON
+                same, why = False, str(e)[:80]
+            ok = R.all_true(same)
+        if ok:
+            xchg, exchange = x, "p2p_fused_exchange"
+        else:
+            if x is not None:
+                try:
+                    x.close()
+                except Exception:
+                    pass
+            exchange = f"{R.backend}_allreduce" + (f" (p2p setup failed: {why})" if why else "")
 
     def step(ev_k0=None, ev_k1=None):
         with torch.cuda.stream(stream):
