@@ -1,3 +1,5 @@
+"""Probe: general (sorted-distinct) f32 path on uniform random 256^3 / 512^3
+volumes -- wall time of ctx.vcec and parity against the oracle."""
 import sys, os, time
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch

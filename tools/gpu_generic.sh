@@ -1,4 +1,5 @@
 #!/bin/bash
+# Generic (tournament) kernels: timing probe + the full GPU suite.
 TAG=${1:-g}
 mkdir -p gpurun_out
 timeout 300 python tools/probe_generic.py > gpurun_out/${TAG}_probe.jsonl 2>&1

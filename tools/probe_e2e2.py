@@ -1,3 +1,5 @@
+"""Probe: end-to-end C2 (512^3 u8 from pinned host memory) through the
+Python API, the overlapped H2D + kernel path, against the device-resident time."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
