@@ -11,7 +11,8 @@
 // Mapping.  Rows run along axis 0, pixels of a row along axis 1.  A lane
 // owns a 32-pixel chunk of a row (bit p = pixel 32c + p) and a warp holds 32
 // consecutive chunks of the same row; lanes 0 and 31 are halo, so a warp
-// "strip" is 30 chunks (960 pixels) wide.  A work unit is (band of rows,
+// "strip" is 30 chunks (960 pixels) wide.  Rows of at most 16 chunks are
+// packed instead (PACK): L lanes per whole row, 32 / L rows per warp.  A work unit is (band of rows,
 // strip), band-major, so warps running together read neighbouring strips of
 // the same rows and the halo chunks / rows hit in L2.  The warp sweeps its
 // band row by row (one row prefetched ahead, two 16-byte loads per lane).
@@ -70,7 +71,8 @@ struct Geom {
   int nchunks;          // 32-pixel chunks per row
   int nstrips;          // warps across a row
   int band;             // rows per unit
-  int nunits;           // bands * nstrips
+  int nunits;           // bands * nstrips (strips); ceil(bands / G) (packed rows)
+  int L, G;             // packed rows: lanes per row (a power of two >= nchunks), rows per warp
   uint32_t four;        // = 4, opaque to ptxas (IMAD address, not an ALU LEA)
 };
 
@@ -103,7 +105,13 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   return v;
 }
 
-template <bool CLUSTER>
+// PACK: rows of at most 16 chunks are packed G = 32 / L to a warp (L lanes
+// per row, no halo lanes: the whole row is in the warp), each lane group
+// sweeping its own band; otherwise a warp holds a strip of 30 chunks of one
+// row between two halo lanes.  CLUSTER: units are dealt round-robin over the
+// CTAs (few warps per SM for a small image) and the curve is reduced in the
+// cluster (fin_u8.cuh, cluster_finalize).
+template <bool CLUSTER, bool PACK>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_u8_2d(const Geom g, int64_t* __restrict__ ghist, const u8fin::Fin fin) {
   if constexpr (CLUSTER) u8fin::cluster_started_arrive();
@@ -114,16 +122,32 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
   const int nwt = gridDim.x * NW;
   const uint32_t hist_s = smem_u32(hist) + (uint32_t)(((threadIdx.x & 31) * HREP) >> 5) * 4u;
 
-  for (int u = blockIdx.x * NW + warp; u < g.nunits; u += nwt) {
-    const int bi = u / g.nstrips, strip = u - bi * g.nstrips;
-    const int R0 = g.own0 + bi * g.band;
-    const int rows = min(g.band, g.own0 + g.P - R0);
-    const int c = strip * STRIP - 1 + lane;  // this lane's chunk (may be -1 or >= nchunks)
+  const int W = PACK ? g.L : 32;  // shuffle width: the lanes of one row
+  for (int u = CLUSTER ? warp * gridDim.x + blockIdx.x : blockIdx.x * NW + warp; u < g.nunits;
+       u += nwt) {
+    int R0, rows, c, steps;
+    if constexpr (PACK) {
+      const int grp = lane / g.L;
+      c = lane - grp * g.L;
+      R0 = g.own0 + (u * g.G + grp) * g.band;
+      rows = max(0, min(g.band, g.own0 + g.P - R0));  // 0: a group past the last band
+      steps = g.band;                                 // warp-uniform sweep length
+    } else {
+      const int bi = u / g.nstrips, strip = u - bi * g.nstrips;
+      R0 = g.own0 + bi * g.band;
+      rows = min(g.band, g.own0 + g.P - R0);
+      c = strip * STRIP - 1 + lane;  // this lane's chunk (may be -1 or >= nchunks)
+      steps = rows;
+    }
     const int lo = 32 * c;
     uint32_t zout = FULL;  // pixels of the chunk outside [0, W1)
     if (c >= 0 && c < g.nchunks) zout = (g.W1 - lo >= 32) ? 0u : (FULL << (g.W1 - lo));
-    const uint32_t vm = (lane >= 1 && lane <= STRIP) ? ~zout : 0u;
+    const uint32_t vm = PACK ? (c < g.nchunks ? ~zout : 0u) : ((lane >= 1 && lane <= STRIP) ? ~zout : 0u);
     const bool first = c == 0;
+    // packed rows: the last lane of a row group has no right neighbour lane
+    // (the row's right collar, which never wins as the later side)
+    const uint32_t rcol = (PACK && c == g.L - 1) ? 1u : 0u;
+    const int Rend = R0 + rows;
     const bool chunk_in = c >= 0 && c < g.nchunks;
     const bool hi_in = lo + 16 < g.W1;  // the chunk's second 16 bytes hold image pixels
 
@@ -166,7 +190,10 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
       {
         uint32_t t[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) t[i] = __funnelshift_r(C[i], __shfl_down_sync(FULL, C[i], 1), 1);
+        for (int i = 0; i < 8; ++i) {
+          t[i] = __funnelshift_r(C[i], __shfl_down_sync(FULL, C[i], 1, W), 1);
+          if constexpr (PACK) t[i] |= rcol << 31;
+        }
         N.gz = bits::gt<8>(C, t);
         bits::sel<8>(N.mz, N.gz, C, t);
       }
@@ -177,12 +204,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         // the quad anchored one pixel to the left: from the previous chunk,
         // or for chunk 0 the quad over the left collar, whose minima are the
         // pixels at 0 -- its comparison is gx bit 0
-        uint32_t qprev = __shfl_up_sync(FULL, gq, 1);
+        uint32_t qprev = __shfl_up_sync(FULL, gq, 1, W);
         if (first) qprev = gx << 31;
         const uint32_t gq1 = __funnelshift_l(qprev, gq, 1);
         if constexpr (K == 2) {
-          const uint32_t vmr = (X - 1 < g.W0) ? vm : 0u;
-          uint32_t zprev = __shfl_up_sync(FULL, P.gz, 1);
+          const uint32_t vmr = (X - 1 < g.W0 && X - 1 < Rend) ? vm : 0u;
+          uint32_t zprev = __shfl_up_sync(FULL, P.gz, 1, W);
           if (first) zprev = FULL;  // column -1 never wins
           if (vmr) {
             const uint32_t Z0 = ~P.gz;
@@ -220,12 +247,12 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     };
     step(R0 - 1, B, A, std::integral_constant<int, 0>{});
     step(R0, A, B, std::integral_constant<int, 1>{});
-    int X = R0 + 1;
-    for (; X + 1 <= R0 + rows; X += 2) {
-      step(X, B, A, std::integral_constant<int, 2>{});
-      step(X + 1, A, B, std::integral_constant<int, 2>{});
+    int t = 1;  // rows R0 + t arrive; the sweep length is warp-uniform
+    for (; t + 1 <= steps; t += 2) {
+      step(R0 + t, B, A, std::integral_constant<int, 2>{});
+      step(R0 + t + 1, A, B, std::integral_constant<int, 2>{});
     }
-    if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
+    if (t <= steps) step(R0 + t, B, A, std::integral_constant<int, 2>{});
   }
   if constexpr (CLUSTER) {
     extern __shared__ __align__(16) int cluster_rows[];
@@ -264,71 +291,99 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
     fin.x = u8fin::Xchg{fz->world, fz->rank, fz->epoch, fz->slots, fz->flags, fz->my_slots,
                         fz->my_flags, fz->err};
   }
+  // rows of <= 16 chunks: packed, G = 32 / L rows per warp
+#ifndef ECC_U82D_PACK
+#define ECC_U82D_PACK 1
+#endif
+  const bool pack = ECC_U82D_PACK && g.nchunks <= 16;
+  g.L = 1;
+  while (g.L < g.nchunks) g.L *= 2;
+  g.G = pack ? 32 / g.L : 1;
+  if (!pack) g.L = 32;
+  // band slots one unit covers: strips -> 1 / nstrips of a band, packed -> G bands
+  auto units_of = [&](long long band) {
+    const long long nbands = (g.P + band - 1) / band;
+    return pack ? (nbands + g.G - 1) / g.G : nbands * g.nstrips;
+  };
   // Small images with the fused curve on one GPU (C1): all CTAs in one
-  // thread-block cluster, the curve reduced over distributed shared memory
-  // (fin_u8.cuh, cluster_finalize) -- bands of up to 4 rows so the units fit
-  // one cluster of the largest size this kernel can be co-scheduled with.
+  // thread-block cluster, units dealt round-robin over the CTAs, the curve
+  // reduced over distributed shared memory (fin_u8.cuh, cluster_finalize) --
+  // bands of up to 4 rows so the units fit one cluster of the largest size
+  // this kernel can be co-scheduled with.
   static int max_cluster = -1;  // same on every B200
   if (max_cluster < 0) {
     max_cluster = 0;
-    if (cudaFuncSetAttribute(k_u8_2d<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) ==
-            cudaSuccess &&
-        cudaFuncSetAttribute(k_u8_2d<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             u8fin::cluster_rows_bytes) == cudaSuccess) {
+    bool ok = true;
+    for (auto k : {k_u8_2d<true, false>, k_u8_2d<true, true>})
+      ok = ok &&
+           cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                u8fin::cluster_rows_bytes) == cudaSuccess;
+    if (ok) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(u8fin::kMaxCluster);
       q.blockDim = dim3(NT);
       q.dynamicSmemBytes = u8fin::cluster_rows_bytes;
       int cs = 0;
-      if (cudaOccupancyMaxPotentialClusterSize(&cs, k_u8_2d<true>, &q) == cudaSuccess)
+      if (cudaOccupancyMaxPotentialClusterSize(&cs, k_u8_2d<true, false>, &q) == cudaSuccess)
         max_cluster = std::min(cs, u8fin::kMaxCluster);
     }
     (void)cudaGetLastError();
   }
   if (fz && fz->world <= 1 && max_cluster >= 2 && g.P > 0 && (long long)g.P * g.W1 <= (1ll << 22)) {
     const long long cap_units = (long long)max_cluster * NW;
-    if (g.nstrips <= cap_units) {
-      const long long per = cap_units / g.nstrips;  // bands that fit the cluster
-      const long long band = (g.P + per - 1) / per;
-      if (band <= 4) {
-        Geom gc = g;
-        gc.band = (int)band;
-        gc.nunits = (int)((g.P + band - 1) / band * g.nstrips);
-        const unsigned grid = (unsigned)((gc.nunits + NW - 1) / NW);
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(NT);
-        cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
-        cfg.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = grid;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        if (cudaLaunchKernelEx(&cfg, k_u8_2d<true>, gc, ghist, fin) == cudaSuccess) return cudaSuccess;
-        // the cluster could not be placed (e.g. SMs held by other work): the
-        // regular launch below computes the same curve
-        (void)cudaGetLastError();
-      }
+    long long band = 1;
+    while (band <= 4 && units_of(band) > cap_units) ++band;
+    if (band <= 4) {
+      Geom gc = g;
+      gc.band = (int)band;
+      gc.nunits = (int)units_of(band);
+      const unsigned grid = (unsigned)std::min<long long>(max_cluster, gc.nunits);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = grid;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const cudaError_t e = pack ? cudaLaunchKernelEx(&cfg, k_u8_2d<true, true>, gc, ghist, fin)
+                                 : cudaLaunchKernelEx(&cfg, k_u8_2d<true, false>, gc, ghist, fin);
+      if (e == cudaSuccess) return cudaSuccess;
+      // the cluster could not be placed (e.g. SMs held by other work): the
+      // regular launch below computes the same curve
+      (void)cudaGetLastError();
     }
   }
   const long long cap_warps = (long long)sms * CTAS_PER_SM * NW;
   // bands of >= 32 rows (2 halo rows per band); ~4 units per resident warp
   // when the image is large enough, else one wave of shorter bands (>= MINBAND:
   // small images are latency-bound, so more, shorter bands finish sooner)
-  long long nb = std::max<long long>(1, (4 * cap_warps) / g.nstrips);
-  long long band = std::max<long long>(32, (g.P + nb - 1) / nb);
-  if ((long long)((g.P + band - 1) / band) * g.nstrips < cap_warps)
-    band = std::max<long long>(MINBAND, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
+  long long band;
+  if (!pack) {
+    const long long nb = std::max<long long>(1, (4 * cap_warps) / g.nstrips);
+    band = std::max<long long>(32, (g.P + nb - 1) / nb);
+    if ((long long)((g.P + band - 1) / band) * g.nstrips < cap_warps)
+      band = std::max<long long>(MINBAND, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
+  } else {
+    const long long slots = cap_warps * g.G;  // bands in one wave of warps
+    band = std::max<long long>(32, (g.P + 4 * slots - 1) / (4 * slots));
+    if ((g.P + band - 1) / band < slots) band = std::max<long long>(MINBAND, (g.P + slots - 1) / slots);
+  }
   band = std::max<long long>(1, std::min<long long>(band, std::max(1, g.P)));
   g.band = (int)band;
-  const long long units = (g.P + band - 1) / band * g.nstrips;
+  const long long units = units_of(band);
   if (g.P <= 0 || units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
   const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
-  k_u8_2d<false><<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
+  if (pack)
+    k_u8_2d<false, true><<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
+  else
+    k_u8_2d<false, false><<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
   return cudaGetLastError();
 }
 

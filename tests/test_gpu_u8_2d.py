@@ -152,3 +152,33 @@ def test_cluster_path_interleaved_with_large_images(ctx):
         assert np.array_equal(bins[:m].cpu().numpy().astype(np.int64), v.astype(np.int64)), shape
         assert np.array_equal(chg[:m].cpu().numpy(), c), shape
         assert np.array_equal(chi[:m].cpu().numpy(), np.cumsum(c)), shape
+
+
+@pytest.mark.parametrize("w", [1, 31, 32, 33, 64, 96, 128, 160, 256, 480, 512])
+def test_packed_rows(ctx, w):
+    """Rows of <= 16 chunks run packed, 32 / L rows per warp (L lanes a row,
+    L a power of two >= the chunk count; the last lane of a full group has
+    the row's right collar as its neighbour).  Heights leave the last warp's
+    row groups partly empty; both the single-launch curve (small images: the
+    cluster path) and slab accumulation (the regular grid) are checked."""
+    import torch
+    rng = np.random.default_rng(w)
+    for h in (1, 2, 3, 5, 33, 257, 1031):
+        img = rng.integers(0, 256, (h, w)).astype(np.uint8)
+        if h % 2:
+            img[:, :: max(1, w // 3)] = 255  # ties with the collar value
+        _check(ctx, img)
+        want = oracle.vcec(img)
+        dev = torch.from_numpy(img).cuda()
+        hist = torch.zeros(512, dtype=torch.int64, device="cuda")
+        dims = eb.Dims.of(img.shape)
+        cut = h // 2
+        for own0, own1 in [(0, cut), (cut, h)]:
+            if own1 > own0:
+                p0, p1 = max(own0 - 1, 0), min(own1 + 1, h)
+                ctx.accumulate_slab(dev[p0:p1].contiguous(), dims, p0, own0, own1, hist)
+        torch.cuda.synchronize()
+        hh = hist.cpu().numpy()
+        bins = np.nonzero(hh[256:])[0]
+        assert np.array_equal(bins, want[0].astype(np.int64)), (h, w)
+        assert np.array_equal(hh[bins], want[1]), (h, w)
