@@ -256,5 +256,57 @@ __device__ __forceinline__ void cluster_finalize(const uint32_t* hist, int* rows
   if (threadIdx.x == 0) *fin.count = (uint64_t)total.x;
 }
 
+// A batch of images, one thread-block cluster per image (k_u8_2d's BATCH
+// path): the same reduction into CTA 0, which writes the image's dense row
+// chi[v] = sum_{v' <= v} change sums (int32, every value 0..255) and its
+// occupancy bitmap -- the batched output format of k_batch.cu.
+template <int NT, class Code, int REP = 1>
+__device__ __forceinline__ void batch_finalize(const uint32_t* hist, int* rows, int32_t* chi_row,
+                                               uint32_t* pres_row) {
+  static_assert(NT >= 256, "one thread per value");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  int(*rows_s)[256] = reinterpret_cast<int(*)[256]>(rows);
+  int(*rows_c)[256] = reinterpret_cast<int(*)[256]>(rows + kMaxCluster * 256);
+  const unsigned rank = cluster.block_rank(), nb = cluster.num_blocks();
+  __syncthreads();
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // CTA 0 has started
+  for (int v = threadIdx.x; v < 256; v += NT) {
+    int sum = 0, cnt = 0;
+#pragma unroll
+    for (int c = 0; c < Code::n; ++c) {
+      if (!Code::live(c)) continue;
+      int n = 0;
+#pragma unroll
+      for (int r = 0; r < REP; ++r) n += (int)hist[(c * 256 + v) * REP + r];
+      cnt += n;
+      sum += n * Code::change(c);
+    }
+    *cluster.map_shared_rank(&rows_s[rank][v], 0) = sum;
+    *cluster.map_shared_rank(&rows_c[rank][v], 0) = cnt;
+  }
+  cluster.sync();
+  if (rank != 0) return;
+  using Scan = cub::BlockScan<int32_t, NT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int v = threadIdx.x;
+  int32_t s = 0, n = 0;
+  if (v < 256) {
+#pragma unroll
+    for (int r = 0; r < kMaxCluster; ++r)
+      if (r < (int)nb) {
+        s += rows_s[r][v];
+        n += rows_c[r][v];
+      }
+  }
+  int32_t incl;
+  Scan(tmp).InclusiveSum(s, incl);
+  if (v < 256) {
+    chi_row[v] = incl;
+    const uint32_t word = __ballot_sync(0xFFFFFFFFu, n != 0);
+    if ((v & 31) == 0) pres_row[v >> 5] = word;
+  }
+}
+
 }  // namespace u8fin
 }  // namespace eccb

@@ -148,6 +148,8 @@ __global__ void __launch_bounds__(NT, 1)
 }
 
 bool batch16_supported(int h, int w);
+cudaError_t launch_batch_u8(const uint8_t* data, uint64_t count, int h, int w, int32_t* chi,
+                            uint32_t* presence, cudaStream_t st);
 cudaError_t launch_batch16(const uint16_t* data, uint64_t count, int h, int w, int32_t* chi,
                            uint32_t* presence, int32_t* spill_scratch, cudaStream_t st);
 
@@ -156,6 +158,10 @@ cudaError_t launch_batch2d(const void* data, int dtype, uint64_t count, int h, i
                            cudaStream_t st) {
   if (count == 0) return cudaSuccess;
   if (dtype == 0) {
+    // rows of a multiple of 16 bytes: the bit-sliced kernel (k_u8_2d.cu)
+    const cudaError_t e = launch_batch_u8(static_cast<const uint8_t*>(data), count, h, w, chi,
+                                          presence, st);
+    if (e != cudaErrorNotSupported) return e;
     const uint32_t nbins = 256;
     const size_t smem = (nbins + nbins / 32) * 4;
     k_batch2d<uint8_t, false><<<(unsigned)count, NT, smem, st>>>(

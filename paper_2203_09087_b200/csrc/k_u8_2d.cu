@@ -74,6 +74,9 @@ struct Geom {
   int nunits;           // bands * nstrips (strips); ceil(bands / G) (packed rows)
   int L, G;             // packed rows: lanes per row (a power of two >= nchunks), rows per warp
   uint32_t four;        // = 4, opaque to ptxas (IMAD address, not an ALU LEA)
+  long long img_stride;  // BATCH: bytes between images (image blockIdx.y)
+  int32_t* chi;          // BATCH: dense rows [count][256]
+  uint32_t* pres;        // BATCH: occupancy bitmaps [count][8]
 };
 
 #ifndef ECC_U82D_MINBAND
@@ -111,10 +114,12 @@ __device__ __forceinline__ uint4 ldg_stream(const void* p) {
 // row between two halo lanes.  CLUSTER: units are dealt round-robin over the
 // CTAs (few warps per SM for a small image) and the curve is reduced in the
 // cluster (fin_u8.cuh, cluster_finalize).
-template <bool CLUSTER, bool PACK>
+template <bool CLUSTER, bool PACK, bool BATCH = false>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     k_u8_2d(const Geom g, int64_t* __restrict__ ghist, const u8fin::Fin fin) {
-  if constexpr (CLUSTER) u8fin::cluster_started_arrive();
+  if constexpr (CLUSTER || BATCH) u8fin::cluster_started_arrive();
+  // BATCH: image blockIdx.y, one thread-block cluster (gridDim.x CTAs) per image
+  const uint8_t* const base = BATCH ? g.base + (size_t)blockIdx.y * g.img_stride : g.base;
   __shared__ __align__(16) uint32_t hist[HIST_WORDS];
   for (int i = threadIdx.x; i < HIST_WORDS; i += NT) hist[i] = 0;
   __syncthreads();
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
         for (int j = 0; j < 8; ++j) W[j] = FULL;
         return;
       }
-      const uint8_t* p = g.base + (long long)(i - g.plane0) * g.pitch + lo;
+      const uint8_t* p = base + (long long)(i - g.plane0) * g.pitch + lo;
       const uint4 a = ldg_stream(p);
       W[0] = a.x; W[1] = a.y; W[2] = a.z; W[3] = a.w;
       if (hi_in) {
@@ -254,8 +259,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     }
     if (t <= steps) step(R0 + t, B, A, std::integral_constant<int, 2>{});
   }
-  if constexpr (CLUSTER) {
-    extern __shared__ __align__(16) int cluster_rows[];
+  extern __shared__ __align__(16) int cluster_rows[];
+  if constexpr (BATCH) {
+    u8fin::batch_finalize<NT, Codes, HREP>(hist, cluster_rows, g.chi + (size_t)blockIdx.y * 256,
+                                          g.pres + (size_t)blockIdx.y * 8);
+  } else if constexpr (CLUSTER) {
     u8fin::cluster_finalize<NT, Codes, HREP>(hist, cluster_rows, fin);
   } else {
     u8fin::flush_and_finalize<NT, Codes, HREP>(hist, ghist, fin);
@@ -385,6 +393,82 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   else
     k_u8_2d<false, false><<<(unsigned)grid, NT, 0, st>>>(g, ghist, fin);
   return cudaGetLastError();
+}
+
+// A batch of 2D u8 images (ecc_batch2d): one thread-block cluster of k CTAs
+// per image (k > 1 only when the batch is too small to fill the GPU), rows
+// packed or in strips as for one image, the dense chi row and occupancy
+// bitmap written by the cluster's CTA 0 (fin_u8.cuh, batch_finalize).
+// Needs rows of a multiple of 16 bytes (16-byte loads); returns
+// cudaErrorNotSupported otherwise (the caller runs k_batch.cu).
+cudaError_t launch_batch_u8(const uint8_t* data, uint64_t count, int h, int w, int32_t* chi,
+                            uint32_t* presence, cudaStream_t st) {
+  using namespace u82d;
+  if (w % 16 != 0 || (reinterpret_cast<uintptr_t>(data) % 16) != 0 || count > 65535u * 1024u ||
+      (long long)h * w > (1ll << 26))
+    return cudaErrorNotSupported;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+    if (cudaFuncSetAttribute(k_u8_2d<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             u8fin::cluster_rows_bytes) != cudaSuccess ||
+        cudaFuncSetAttribute(k_u8_2d<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             u8fin::cluster_rows_bytes) != cudaSuccess)
+      sms = -1;
+    (void)cudaGetLastError();
+  }
+  if (sms < 0) return cudaErrorNotSupported;
+  Geom g{};
+  g.base = data;
+  g.pitch = w;
+  g.W0 = h;
+  g.W1 = w;
+  g.plane0 = 0;
+  g.nheld = h;
+  g.own0 = 0;
+  g.P = h;
+  g.nchunks = (w + 31) / 32;
+  g.nstrips = (g.nchunks + STRIP - 1) / STRIP;
+  g.four = 4 * HREP;
+  g.img_stride = (long long)h * w;
+  g.chi = chi;
+  g.pres = presence;
+  const bool pack = ECC_U82D_PACK && g.nchunks <= 16;
+  g.L = 1;
+  while (g.L < g.nchunks) g.L *= 2;
+  g.G = pack ? 32 / g.L : 1;
+  if (!pack) g.L = 32;
+  // CTAs per image: enough images per wave to fill the GPU, else up to 8 per image
+  const long long k = std::max<long long>(1, std::min<long long>(8, (2 * sms + (long long)count - 1) /
+                                                                      (long long)count));
+  // bands so the image's units fill its k x NW warps once (>= 8 rows a band)
+  const long long warps = k * NW;
+  long long band;
+  if (pack)
+    band = std::max<long long>(std::min<long long>(8, h), (h + warps * g.G - 1) / (warps * g.G));
+  else
+    band = std::max<long long>(std::min<long long>(8, h), ((long long)h * g.nstrips + warps - 1) / warps);
+  g.band = (int)band;
+  const long long nbands = (h + band - 1) / band;
+  g.nunits = (int)(pack ? (nbands + g.G - 1) / g.G : nbands * g.nstrips);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)k, (unsigned)count);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)k;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const u8fin::Fin fin{};
+  return pack ? cudaLaunchKernelEx(&cfg, k_u8_2d<false, true, true>, g, (int64_t*)nullptr, fin)
+              : cudaLaunchKernelEx(&cfg, k_u8_2d<false, false, true>, g, (int64_t*)nullptr, fin);
 }
 
 }  // namespace eccb

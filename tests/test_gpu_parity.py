@@ -596,3 +596,32 @@ def test_f32_more_distinct_values_than_the_first_capacity(ctx):
     assert np.array_equal(np.asarray(got.values), v) and np.array_equal(np.asarray(got.changes), c)
     cur = ctx.curve(img)
     assert np.array_equal(np.asarray(cur.chi), np.cumsum(c))
+
+
+@pytest.mark.parametrize("count,h,w", [(9, 37, 32), (3, 1, 16), (5, 300, 48), (2, 64, 512),
+                                       (1, 700, 1024), (4, 33, 2000), (300, 17, 64),
+                                       (2, 1000, 96)])
+def test_batch2d_u8_bit_sliced(ctx, count, h, w):
+    """u8 batches whose rows are a multiple of 16 bytes run the bit-sliced
+    k_u8_2d kernel, one thread-block cluster per image (several CTAs per
+    image when the batch is small; rows packed or in strips by width); the
+    dense chi rows and occupancy bitmaps match the oracle image by image --
+    random values, ties at the collar value 255, and the dense row format
+    (every value 0..255, absent ones carrying the running sum)."""
+    import torch
+    rng = np.random.default_rng(count * 1000 + w)
+    imgs = rng.integers(0, 256, (count, h, w)).astype(np.uint8)
+    imgs[:, :, ::5] = 255
+    imgs[count // 2] = rng.integers(0, 3, (h, w))  # few values: long runs of absent ones
+    for src in (imgs, torch.from_numpy(imgs).cuda()):
+        chi, pres = ctx.batch2d(src)
+        if not isinstance(chi, np.ndarray):
+            torch.cuda.synchronize()
+            chi, pres = chi.cpu().numpy(), pres.cpu().numpy().view(np.uint32)
+        for b in range(count):
+            v, c = oracle.vcec(imgs[b])
+            dense = np.zeros(256, np.int64)
+            dense[v.astype(np.int64)] = c
+            assert np.array_equal(chi[b].astype(np.int64), np.cumsum(dense)), (b, h, w)
+            bits = np.unpackbits(pres[b].astype("<u4").view(np.uint8), bitorder="little")[:256]
+            assert np.array_equal(np.nonzero(bits)[0], v.astype(np.int64)), (b, h, w)

@@ -88,6 +88,17 @@ v, c = oracle.vcec(imgs8[1])
 good = np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
 ok &= good
 print(("ok  " if good else "BAD ") + "batch2d u8", flush=True)
+# rows of a multiple of 16 bytes: the bit-sliced batch (clusters of several
+# CTAs per image for a small batch), packed rows and strips
+for shp in ((5, 40, 64), (2, 70, 1024)):
+    imgs8 = rng.integers(0, 256, shp).astype(np.uint8)
+    chi, pres = ctx.batch2d(imgs8)
+    for b in range(shp[0]):
+        t, cc = eb.curve_batch_to_points(chi[b], pres[b])
+        v, c = oracle.vcec(imgs8[b])
+        good = np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, np.cumsum(c))
+        ok &= good
+    print(("ok  " if good else "BAD ") + f"batch2d u8 bit-sliced {shp}", flush=True)
 img = rng.integers(0, 256, (6, 20, 32)).astype(np.uint8)
 dev = torch.from_numpy(img).cuda()
 out = torch.empty(img.size, dtype=torch.int8, device="cuda")
