@@ -404,8 +404,7 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
 cudaError_t launch_batch_u8(const uint8_t* data, uint64_t count, int h, int w, int32_t* chi,
                             uint32_t* presence, cudaStream_t st) {
   using namespace u82d;
-  if (w % 16 != 0 || (reinterpret_cast<uintptr_t>(data) % 16) != 0 || count > 65535u * 1024u ||
-      (long long)h * w > (1ll << 26))
+  if (w % 16 != 0 || (reinterpret_cast<uintptr_t>(data) % 16) != 0 || (long long)h * w > (1ll << 26))
     return cudaErrorNotSupported;
   static int sms = 0;
   if (!sms) {
@@ -454,21 +453,32 @@ cudaError_t launch_batch_u8(const uint8_t* data, uint64_t count, int h, int w, i
   g.band = (int)band;
   const long long nbands = (h + band - 1) / band;
   g.nunits = (int)(pack ? (nbands + g.G - 1) / g.G : nbands * g.nstrips);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)k, (unsigned)count);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (unsigned)k;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
   const u8fin::Fin fin{};
-  return pack ? cudaLaunchKernelEx(&cfg, k_u8_2d<false, true, true>, g, (int64_t*)nullptr, fin)
-              : cudaLaunchKernelEx(&cfg, k_u8_2d<false, false, true>, g, (int64_t*)nullptr, fin);
+  // grid.y holds at most 65535 images: larger batches in slices
+  for (uint64_t i0 = 0; i0 < count; i0 += 65535) {
+    const uint64_t n = std::min<uint64_t>(65535, count - i0);
+    Geom gi = g;
+    gi.base = data + i0 * (uint64_t)g.img_stride;
+    gi.chi = chi + i0 * 256;
+    gi.pres = presence + i0 * 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)k, (unsigned)n);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)k;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e =
+        pack ? cudaLaunchKernelEx(&cfg, k_u8_2d<false, true, true>, gi, (int64_t*)nullptr, fin)
+             : cudaLaunchKernelEx(&cfg, k_u8_2d<false, false, true>, gi, (int64_t*)nullptr, fin);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace eccb

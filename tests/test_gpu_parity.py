@@ -625,3 +625,18 @@ def test_batch2d_u8_bit_sliced(ctx, count, h, w):
             assert np.array_equal(chi[b].astype(np.int64), np.cumsum(dense)), (b, h, w)
             bits = np.unpackbits(pres[b].astype("<u4").view(np.uint8), bitorder="little")[:256]
             assert np.array_equal(np.nonzero(bits)[0], v.astype(np.int64)), (b, h, w)
+
+
+def test_batch2d_u8_more_images_than_grid_y(ctx):
+    """More than 65535 images (the grid's y limit): the bit-sliced batch is
+    launched in slices; images on both sides of the cut are exact."""
+    import torch
+    rng = np.random.default_rng(3)
+    imgs = rng.integers(0, 256, (70001, 3, 16)).astype(np.uint8)
+    chi, pres = ctx.batch2d(torch.from_numpy(imgs).cuda())
+    torch.cuda.synchronize()
+    chi, pres = chi.cpu().numpy(), pres.cpu().numpy().view(np.uint32)
+    for b in (0, 1, 65534, 65535, 65536, 70000):
+        t, cc = eb.curve_batch_to_points(chi[b], pres[b])
+        v, c = oracle.curve(imgs[b])
+        assert np.array_equal(t, v.astype(np.int64)) and np.array_equal(cc, c), b
