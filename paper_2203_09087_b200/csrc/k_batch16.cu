@@ -295,53 +295,59 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (X <= R0 + rows) step(X, B, A, std::integral_constant<int, 2>{});
   __syncthreads();
-  // epilogue, conflict-free: warp w owns a contiguous run of 128-bin chunks
-  // (32 for 16 warps); lane l holds 4 consecutive bins of a chunk (one 8-byte
-  // shared load, the chunk's spill bits one broadcast word).  Pass 1 sums the
-  // warp's bins, pass 2 scans chunk by chunk and writes chi coalesced.
-  // warp w owns the 128-bin chunks [c0, c1) (contiguous, in order)
-  const uint32_t c0 = (uint32_t)warp * 512u / NW, c1 = (uint32_t)(warp + 1) * 512u / NW;
+  // epilogue, conflict-free: warp w owns a contiguous run of 256-bin chunks
+  // (16 for 16 warps); lane l holds 8 consecutive bins of a chunk (one
+  // 16-byte shared load, the chunk's spill bits one broadcast word).  Pass 1
+  // sums the warp's bins, pass 2 scans chunk by chunk and writes chi
+  // coalesced (two 16-byte stores per lane).
+  const uint32_t c0 = (uint32_t)warp * 256u / NW, c1 = (uint32_t)(warp + 1) * 256u / NW;
   int32_t* row = chi + (size_t)blockIdx.x * 65536;
-  auto sums4 = [&](uint32_t b, int (&x)[4]) {  // b % 4 == 0
-    const uint2 w2 = *reinterpret_cast<const uint2*>(hw + (b >> 1));
-    x[0] = hist16::lo_value(w2.x);
-    x[1] = hist16::hi_value(w2.x);
-    x[2] = hist16::lo_value(w2.y);
-    x[3] = hist16::hi_value(w2.y);
-    const uint32_t sp = (spilled[b >> 5] >> (b & 31)) & 0xFu;
+  auto sums8 = [&](uint32_t b, int (&x)[8]) {  // b % 8 == 0
+    const uint4 w4 = *reinterpret_cast<const uint4*>(hw + (b >> 1));
+    x[0] = hist16::lo_value(w4.x);
+    x[1] = hist16::hi_value(w4.x);
+    x[2] = hist16::lo_value(w4.y);
+    x[3] = hist16::hi_value(w4.y);
+    x[4] = hist16::lo_value(w4.z);
+    x[5] = hist16::hi_value(w4.z);
+    x[6] = hist16::lo_value(w4.w);
+    x[7] = hist16::hi_value(w4.w);
+    const uint32_t sp = (spilled[b >> 5] >> (b & 31)) & 0xFFu;
     if (sp) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 8; ++k)
         if ((sp >> k) & 1u) x[k] += scratch[b + k];
     }
   };
   __shared__ int32_t wsum[NW];
-  const uint32_t wb = 4u * lane;
+  const uint32_t wb = 8u * lane;
   int32_t part = 0;
-  for (uint32_t i = c0 * 128u; i < c1 * 128u; i += 128) {
-    int x[4];
-    sums4(wb + i, x);
-    part += x[0] + x[1] + x[2] + x[3];
+  for (uint32_t i = c0 * 256u; i < c1 * 256u; i += 256) {
+    int x[8];
+    sums8(wb + i, x);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part += x[k];
   }
   part = __reduce_add_sync(FULL, part);
   if (lane == 0) wsum[warp] = part;
   __syncthreads();
   int32_t carry = 0;
   for (int j = 0; j < warp; ++j) carry += wsum[j];
-  for (uint32_t i = c0 * 128u; i < c1 * 128u; i += 128) {
-    int x[4];
-    sums4(wb + i, x);
-    x[1] += x[0];
-    x[2] += x[1];
-    x[3] += x[2];
-    int t = x[3];  // inclusive scan of the lane totals
+  for (uint32_t i = c0 * 256u; i < c1 * 256u; i += 256) {
+    int x[8];
+    sums8(wb + i, x);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) x[k] += x[k - 1];
+    int t = x[7];  // inclusive scan of the lane totals
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(FULL, t, o);
       if (lane >= o) t += y;
     }
-    const int base = carry + t - x[3];
-    *reinterpret_cast<int4*>(row + wb + i) = make_int4(base + x[0], base + x[1], base + x[2], base + x[3]);
+    const int base = carry + t - x[7];
+    int4* dst = reinterpret_cast<int4*>(row + wb + i);
+    dst[0] = make_int4(base + x[0], base + x[1], base + x[2], base + x[3]);
+    dst[1] = make_int4(base + x[4], base + x[5], base + x[6], base + x[7]);
     carry += __shfl_sync(FULL, t, 31);
   }
   __syncthreads();  // every read of the scratch row is done
