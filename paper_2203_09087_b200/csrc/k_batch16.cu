@@ -83,8 +83,12 @@ __global__ void __launch_bounds__(NT, 1)
   uint32_t* hw = sm;                    // packed halves
   uint32_t* pres = hw + HWORDS;         // occupancy bits
   uint32_t* spilled = pres + PWORDS;    // bins with a spilled partial in `scratch`
-  for (int i = threadIdx.x; i < HWORDS; i += NT) hw[i] = hist16::BIAS;
-  for (int i = threadIdx.x; i < 2 * PWORDS; i += NT) pres[i] = 0;
+  {  // 16-byte stores (the table is 128 KB: 16 per thread)
+    const uint4 bias = make_uint4(hist16::BIAS, hist16::BIAS, hist16::BIAS, hist16::BIAS);
+    for (int i = threadIdx.x; i < HWORDS / 4; i += NT) reinterpret_cast<uint4*>(hw)[i] = bias;
+    for (int i = threadIdx.x; i < 2 * PWORDS / 4; i += NT)
+      reinterpret_cast<uint4*>(pres)[i] = make_uint4(0, 0, 0, 0);
+  }
   __syncthreads();
   const uint16_t* img = data + (size_t)blockIdx.x * h * w;
   int32_t* scratch = spill_scratch + (size_t)smid() * 65536;
