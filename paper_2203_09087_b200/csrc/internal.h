@@ -25,6 +25,19 @@ inline void smem_optin(int bytes) {
   }
 }
 
+// Allow kernel FN non-portable cluster sizes (up to 16 CTAs), once per device.
+template <auto FN>
+inline void cluster16_optin() {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_relaxed) & bit)) {
+    cudaFuncSetAttribute(FN, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    done.fetch_or(bit);
+  }
+}
+
 // Workspace of the fused single-launch curve (k_u8_3d.cu): `ticket` and the
 // 512-entry int64 histogram must be zero before the launch and are zero
 // again after it.

@@ -318,24 +318,22 @@ cudaError_t launch_u8_2d(const Slab& s, int64_t* ghist, int sms, cudaStream_t st
   // reduced over distributed shared memory (fin_u8.cuh, cluster_finalize) --
   // bands of up to 4 rows so the units fit one cluster of the largest size
   // this kernel can be co-scheduled with.
-  static int max_cluster = -1;  // same on every B200
+  // the opt-ins are per device; the largest co-schedulable cluster is the
+  // same on every B200 (measured once)
+  smem_optin<k_u8_2d<true, false>>(u8fin::cluster_rows_bytes);
+  smem_optin<k_u8_2d<true, true>>(u8fin::cluster_rows_bytes);
+  cluster16_optin<k_u8_2d<true, false>>();
+  cluster16_optin<k_u8_2d<true, true>>();
+  static int max_cluster = -1;
   if (max_cluster < 0) {
-    max_cluster = 0;
-    bool ok = true;
-    for (auto k : {k_u8_2d<true, false>, k_u8_2d<true, true>})
-      ok = ok &&
-           cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
-           cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                u8fin::cluster_rows_bytes) == cudaSuccess;
-    if (ok) {
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(u8fin::kMaxCluster);
-      q.blockDim = dim3(NT);
-      q.dynamicSmemBytes = u8fin::cluster_rows_bytes;
-      int cs = 0;
-      if (cudaOccupancyMaxPotentialClusterSize(&cs, k_u8_2d<true, false>, &q) == cudaSuccess)
-        max_cluster = std::min(cs, u8fin::kMaxCluster);
-    }
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(u8fin::kMaxCluster);
+    q.blockDim = dim3(NT);
+    q.dynamicSmemBytes = u8fin::cluster_rows_bytes;
+    int cs = 0;
+    max_cluster = cudaOccupancyMaxPotentialClusterSize(&cs, k_u8_2d<true, false>, &q) == cudaSuccess
+                      ? std::min(cs, u8fin::kMaxCluster)
+                      : 0;
     (void)cudaGetLastError();
   }
   if (fz && fz->world <= 1 && max_cluster >= 2 && g.P > 0 && (long long)g.P * g.W1 <= (1ll << 22)) {
@@ -412,14 +410,10 @@ cudaError_t launch_batch_u8(const uint8_t* data, uint64_t count, int h, int w, i
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       sms = 148;
-    if (cudaFuncSetAttribute(k_u8_2d<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             u8fin::cluster_rows_bytes) != cudaSuccess ||
-        cudaFuncSetAttribute(k_u8_2d<false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             u8fin::cluster_rows_bytes) != cudaSuccess)
-      sms = -1;
     (void)cudaGetLastError();
   }
-  if (sms < 0) return cudaErrorNotSupported;
+  smem_optin<k_u8_2d<false, true, true>>(u8fin::cluster_rows_bytes);
+  smem_optin<k_u8_2d<false, false, true>>(u8fin::cluster_rows_bytes);
   Geom g{};
   g.base = data;
   g.pitch = w;
