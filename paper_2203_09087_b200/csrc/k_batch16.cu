@@ -327,10 +327,23 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t wb = 8u * lane;
   int32_t part = 0;
   for (uint32_t i = c0 * 256u; i < c1 * 256u; i += 256) {
-    int x[8];
-    sums8(wb + i, x);
+    // lo + hi of a word without unpacking: t = w - BIAS = hi * 65536 + lo
+    // exactly, hi = (t + 32768) >> 16 (arithmetic), so lo + hi = t - 65535 hi
+    // (tests/cpp/test_bits.cpp checks the identity; 1.635 vs 1.644 ms for C3)
+    const uint32_t b = wb + i;
+    const uint4 w4 = *reinterpret_cast<const uint4*>(hw + (b >> 1));
+    const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) part += x[k];
+    for (int q = 0; q < 4; ++q) {
+      const int t = (int)(ws[q] - hist16::BIAS);
+      part += t - 65535 * ((t + 32768) >> 16);
+    }
+    const uint32_t sp = (spilled[b >> 5] >> (b & 31)) & 0xFFu;
+    if (sp) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if ((sp >> k) & 1u) part += scratch[b + k];
+    }
   }
   part = __reduce_add_sync(FULL, part);
   if (lane == 0) wsum[warp] = part;

@@ -100,6 +100,11 @@ static int test_hist16() {
     for (int k = 0; k < 15 + 8; ++k) {
       const int vhi = k < 15 ? edges[k] : (int)(rng() % 65535) - 32767;
       const uint32_t w = BIAS + (uint32_t)vlo + ((uint32_t)vhi << 16);
+      const int t = (int)(w - BIAS);  // k_batch16's pass-1 sum of both halves
+      if (t - 65535 * ((t + 32768) >> 16) != vlo + vhi) {
+        std::printf("hist16 pair sum mismatch %d %d\n", vlo, vhi);
+        return 1;
+      }
       if (lo_value(w) != vlo || hi_value(w) != vhi || half_value(w, 0) != vlo || half_value(w, 1) != vhi) {
         std::printf("hist16 decode mismatch %d %d\n", vlo, vhi);
         return 1;
