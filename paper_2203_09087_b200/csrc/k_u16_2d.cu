@@ -100,7 +100,9 @@ __global__ void __launch_bounds__(NT, 1)
               static_cast<unsigned long long>(static_cast<long long>(after)));
   };
 
-  for (int u = blockIdx.x * NW + warp; u < g.nunits; u += nwt) {
+  // units dealt round-robin over the CTAs: a small image spreads over every
+  // SM (a few warps each) instead of filling a few SMs' 16 warps
+  for (int u = warp * gridDim.x + blockIdx.x; u < g.nunits; u += nwt) {
     const int bi = u / g.nstrips, strip = u - bi * g.nstrips;
     const int R0 = g.own0 + bi * g.band;
     const int rows = min(g.band, g.own0 + g.P - R0);
@@ -259,16 +261,23 @@ cudaError_t launch_u16_2d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   g.nbins = nbins;
   if (g.P <= 0) return cudaErrorInvalidValue;
   const long long cap_warps = (long long)sms * NW;
-  // one wave: bands sized so the units just fill the resident warps (>= 8
-  // rows per band: 2 halo rows each), else several units per warp
-  long long band = std::max<long long>(8, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
-  band = std::min<long long>(band, g.P);
+  // bands of >= 32 rows (2 halo rows each), ~4 units per resident warp when
+  // the image is large, else one wave of shorter bands (>= MINBAND rows: a
+  // small image is latency-bound, so more, shorter bands finish sooner)
+#ifndef ECC_U162D_MINBAND
+#define ECC_U162D_MINBAND 2
+#endif
+  const long long nb = std::max<long long>(1, (4 * cap_warps) / g.nstrips);
+  long long band = std::max<long long>(32, (g.P + nb - 1) / nb);
+  if ((g.P + band - 1) / band * g.nstrips < cap_warps)
+    band = std::max<long long>(ECC_U162D_MINBAND, ((long long)g.P * g.nstrips + cap_warps - 1) / cap_warps);
+  band = std::max<long long>(1, std::min<long long>(band, g.P));
   g.band = (int)band;
   const long long units = (g.P + band - 1) / band * g.nstrips;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
   smem_optin<k_u16_2d>(SMEM_BYTES);
-  const long long grid = std::min<long long>((units + NW - 1) / NW, sms);
+  const long long grid = std::min<long long>(units, sms);
   k_u16_2d<<<(unsigned)grid, NT, SMEM_BYTES, st>>>(g, ghist);
   return cudaGetLastError();
 }
