@@ -103,6 +103,7 @@ struct Geom {
   int nunits;      // ncols * segments
   int8_t* chg;     // CH mode: per-voxel changes of the owned planes (compute_changes)
   uint32_t four;   // = 4, opaque to ptxas so the histogram address stays an IMAD
+  int rr;          // units < resident warps: dealt round-robin over the CTAs (every SM busy)
 };
 
 // Fused K3 (optional, fin_u8.cuh): the last CTA to finish turns the global
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
   __syncthreads();
 
   const int nwt = gridDim.x * NW;
-  const int gw = blockIdx.x * NW + warp;
+  const int gw = g.rr ? warp * (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x * NW + warp;
 
   Cursor pc;
   pc.start(g, gw);
@@ -540,13 +541,23 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
     nseg = std::max<long long>(1, cap_warps / g.ncols);
   else
     nseg = (8 * cap_warps + g.ncols - 1) / g.ncols;
-  nseg = std::min<long long>(nseg, std::max(1, g.P / 8));  // segments of >= 8 planes
+#ifndef ECC_U83D_MINSEG
+#define ECC_U83D_MINSEG 4
+#endif
+  nseg = std::min<long long>(nseg, std::max(1, g.P / ECC_U83D_MINSEG));  // segments of >= MINSEG planes
   g.seglen = (int)((g.P + nseg - 1) / nseg);
   nseg = (g.P + g.seglen - 1) / g.seglen;
   const long long units = nseg * g.ncols;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
-  const long long grid = std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
+#ifndef ECC_U83D_RR
+#define ECC_U83D_RR 1
+#endif
+  // fewer units than resident warps: one unit per warp on as many SMs as
+  // possible (a small volume is latency-bound: a few warps per SM step faster)
+  g.rr = ECC_U83D_RR && units < cap_warps;
+  const long long grid = g.rr ? std::min<long long>(units, cap_warps / NW)
+                              : std::min<long long>((units + NW - 1) / NW, cap_warps / NW);
   Fin fin{};
   if (fz) {
     fin = Fin{fz->ticket, fz->bins, fz->changes, fz->chi, fz->count};
