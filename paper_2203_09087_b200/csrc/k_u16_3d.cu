@@ -63,6 +63,7 @@ static_assert(hist16::no_wrap(NW * 32, GRP, 7), "3D changes reach -7: the packed
 struct Geom {
   int W0, W1, W2, plane0, own0, P, Gy, Gz, ncols, seglen, nunits;
   uint32_t nbins;
+  int rr;  // units < resident warps: dealt round-robin over the CTAs (every SM busy)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -376,7 +377,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   }
   __syncthreads();
   const int nwt = gridDim.x * NW;
-  const int gw = blockIdx.x * NW + warp;
+  const int gw = g.rr ? warp * (int)gridDim.x + (int)blockIdx.x : (int)blockIdx.x * NW + warp;
   Cursor pc;
   pc.start(g, gw);
   auto issue = [&](int slot) {
@@ -501,7 +502,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode16() {
 long long best_segments(long long ncols, long long P, long long cap_warps) {
   long long best = 1;
   double best_cost = 1e300;
-  for (long long n = 1; n <= std::max<long long>(1, P / 8); ++n) {
+  for (long long n = 1; n <= std::max<long long>(1, P / 4); ++n) {  // segments >= 4 planes
     const long long len = (P + n - 1) / n;
     const long long units = ((P + len - 1) / len) * ncols;
     const long long per_warp = (units + cap_warps - 1) / cap_warps;
@@ -560,7 +561,11 @@ cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   const long long units = nseg * g.ncols;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   g.nunits = (int)units;
-  const long long grid = std::min<long long>((units + NW - 1) / NW, sms);
+  // fewer units than resident warps: one unit per warp on as many SMs as
+  // possible (a small volume is latency-bound)
+  g.rr = units < cap_warps;
+  const long long grid = g.rr ? std::min<long long>(units, sms)
+                              : std::min<long long>((units + NW - 1) / NW, sms);
   k_u16_3d<<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
   return cudaGetLastError();
 }
