@@ -734,12 +734,30 @@ __global__ void __launch_bounds__(1024) k_scan_partials(longlong2* part, uint32_
   if (threadIdx.x == 0) *count = (uint64_t)total.x;
 }
 
-template <bool PACKED>
+// SCAN: `part` holds the raw per-block totals (nblk <= T) and every block
+// reduces those of the blocks before it itself -- no k_scan_partials launch;
+// the last block writes the point count.
+template <bool PACKED, bool SCAN = false>
 __global__ void __launch_bounds__(T) k_write(const int64_t* __restrict__ hist, uint32_t nbins,
                                              const longlong2* __restrict__ part, uint32_t* bins,
-                                             int64_t* changes, int64_t* chi) {
+                                             int64_t* changes, int64_t* chi, uint64_t* count = nullptr) {
   using Scan = cub::BlockScan<longlong2, T>;
   __shared__ typename Scan::TempStorage tmp;
+  __shared__ longlong2 base;
+  if constexpr (SCAN) {
+    using Red = cub::BlockReduce<longlong2, T>;
+    __shared__ typename Red::TempStorage rtmp;
+    const longlong2 p = threadIdx.x < blockIdx.x ? part[threadIdx.x] : make_longlong2(0, 0);
+    const longlong2 t = Red(rtmp).Reduce(p, Add2());
+    if (threadIdx.x == 0) {
+      base = t;
+      if (blockIdx.x + 1 == gridDim.x) *count = (uint64_t)(t.x + part[blockIdx.x].x);
+    }
+    __syncthreads();
+  } else {
+    if (threadIdx.x == 0) base = part[blockIdx.x];
+    __syncthreads();
+  }
   const uint32_t b0 = blockIdx.x * B + threadIdx.x * PER;
   long long s[PER], n[PER];
   longlong2 v = make_longlong2(0, 0);
@@ -752,7 +770,7 @@ __global__ void __launch_bounds__(T) k_write(const int64_t* __restrict__ hist, u
   }
   longlong2 ex;
   Scan(tmp).ExclusiveScan(v, ex, make_longlong2(0, 0), Add2());
-  long long pos = part[blockIdx.x].x + ex.x, acc = part[blockIdx.x].y + ex.y;
+  long long pos = base.x + ex.x, acc = base.y + ex.y;
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
     acc += s[i];
@@ -782,6 +800,13 @@ cudaError_t launch_finalize(const int64_t* hist, uint32_t nbins, uint32_t* bins,
     fin::k_partials<true><<<nblk, fin::T, 0, st>>>(hist, nbins, part);
   else
     fin::k_partials<false><<<nblk, fin::T, 0, st>>>(hist, nbins, part);
+  if (nblk <= (uint32_t)fin::T) {  // <= 256 K bins: the prefix of the partials in k_write
+    if (packed)
+      fin::k_write<true, true><<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi, count);
+    else
+      fin::k_write<false, true><<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi, count);
+    return cudaGetLastError();
+  }
   fin::k_scan_partials<<<1, 1024, 0, st>>>(part, nblk, count);
   if (packed)
     fin::k_write<true><<<nblk, fin::T, 0, st>>>(hist, nbins, part, bins, changes, chi);
