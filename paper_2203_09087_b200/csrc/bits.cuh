@@ -71,6 +71,28 @@ __host__ __device__ __forceinline__ uint32_t shr_fma(uint32_t x, int k) {
 #endif
 }
 
+// (x >> 1) + a and (x << 1) + a as ONE FMA-pipe instruction each (IMAD.HI /
+// IMAD with an addend): the shift plus a bit that lands where the shift
+// left a zero (a < 2^31, resp. a in {0, 1}).
+__host__ __device__ __forceinline__ uint32_t shr1_add(uint32_t x, uint32_t a) {
+#ifdef __CUDA_ARCH__
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(0x80000000u), "r"(a));
+  return d;
+#else
+  return (x >> 1) + a;
+#endif
+}
+__host__ __device__ __forceinline__ uint32_t shl1_add(uint32_t x, uint32_t a) {
+#ifdef __CUDA_ARCH__
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(2u), "r"(a));
+  return d;
+#else
+  return (x << 1) + a;
+#endif
+}
+
 // (x >> p) & 1 for a compile-time p on the FMA pipe: IMAD.SHL moves bit p
 // to bit 31, IMAD.HI by 2 brings it down alone.
 __host__ __device__ __forceinline__ uint32_t bit_fma(uint32_t x, int p) {

@@ -151,17 +151,38 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
 // nwt, segment-major) and of the plane step k in [0, len + 2) within it
 // (one halo plane on each side along axis 0); the producer moves a box of
 // PB planes at a time.
+// Column groups along an in-plane axis of width W.  A column's window is 32
+// rows (lanes) / bits; an interior column owns 30 of them (one halo on each
+// side), but the image's first and last columns own 31: the collar beyond
+// the image edge is VIRTUAL (no lane / bit holds it, its comparisons are
+// substituted in sweep_step), so 512 = 31 + 15 x 30 + 31 takes 17 columns
+// instead of 18 (-11 % plane steps at 512^2 per plane).
+__host__ __device__ __forceinline__ int col_groups(int W) {
+  return W <= 32 ? 1 : 2 + (W - 62 + 29) / 30 * (W > 62);
+}
+// First owned index of group k (k = G: W).  W = q G + r; the r groups one
+// voxel larger are taken in the order 0, G-1, 1, 2, ... (only the two edge
+// groups may own 31).
+__host__ __device__ __forceinline__ int col_start(int k, int G, int W) {
+  if (k <= 0) return 0;
+  if (k >= G) return W;
+  const int q = W / G, r = W - q * G;
+  return k * q + (r > 0) + max(0, min(k - 1, r - 2));
+}
+
 struct Cursor {
-  int u, k, len, x0, ys, ye, zs, ze;
+  int u, k, len, x0, ys, ye, zs, ze, yb, zb;  // owned [ys, ye) x [zs, ze); window origin (yb, zb)
   __device__ __forceinline__ void set(const Geom& g) {
     const int seg = u / g.ncols, col = u - seg * g.ncols;
     x0 = g.own0 + seg * g.seglen;
     len = min(g.seglen, g.P - seg * g.seglen);
     const int gy = col / g.Gz, gz = col - gy * g.Gz;
-    ys = (int)((long long)gy * g.W1 / g.Gy);
-    ye = (int)((long long)(gy + 1) * g.W1 / g.Gy);
-    zs = (int)((long long)gz * g.W2 / g.Gz);
-    ze = (int)((long long)(gz + 1) * g.W2 / g.Gz);
+    ys = col_start(gy, g.Gy, g.W1);
+    ye = col_start(gy + 1, g.Gy, g.W1);
+    zs = col_start(gz, g.Gz, g.W2);
+    ze = col_start(gz + 1, g.Gz, g.W2);
+    yb = ys > 0 ? ys - 1 : 0;  // the first column starts at the image edge (virtual collar)
+    zb = zs > 0 ? zs - 1 : 0;
   }
   __device__ __forceinline__ void start(const Geom& g, int u0) {
     u = u0;
@@ -198,24 +219,27 @@ struct RunGeom {
   int o;          // byte offset of the window in the 16-byte aligned box row
   uint32_t zout;  // bits whose voxel lies outside [0, W2)
   uint32_t vm;    // bits whose change this lane emits (0 for halo lanes)
+  uint32_t vlo;   // FULL on lane 0 of a first column: its y - 1 neighbour is the virtual collar
+  uint32_t zf;    // 1 in a first column: bit 0's z - 1 neighbour is the virtual collar
+  uint32_t zl;    // bit 31 in a last column: bit 31's z + 1 neighbour is the virtual collar
   bool yout;      // this lane's row lies outside [0, W1)
-  bool zlo;       // bit 0 is the z = -1 collar
   bool edge;      // some lane of the column holds collar voxels (warp-uniform)
+  bool b0, b31;   // bit 0 / bit 31 owned (first / last columns; warp-uniform)
   __device__ __forceinline__ void set(const Geom& g, const Cursor& c, int lane) {
-    y = c.ys - 1 + lane;
-    const int z0 = c.zs - 1;
-    o = z0 - ((z0 >> 4) << 4);
-    yout = (y < 0) | (y >= g.W1);
-    zlo = z0 < 0;
-    const int lo = -z0;         // first in-image bit
+    y = c.yb + lane;
+    const int z0 = c.zb;
+    o = z0 & 15;
+    yout = y >= g.W1;
     const int hi = g.W2 - z0;   // one past the last in-image bit
-    uint32_t in = FULL;
-    if (lo > 0) in &= FULL << lo;
-    if (hi < 32) in &= (1u << hi) - 1u;
-    zout = ~in;
-    const int nz = c.ze - c.zs;  // owned bits 1..nz
-    const uint32_t own = (nz >= 31 ? FULL : ((1u << (nz + 1)) - 1u)) & ~1u;
-    vm = (lane >= 1 && lane <= c.ye - c.ys) ? own : 0u;
+    zout = hi < 32 ? ~((1u << hi) - 1u) : 0u;
+    const int lo_b = c.zs - z0, hi_b = c.ze - z0;  // owned bits [lo_b, hi_b)
+    const uint32_t own = (hi_b >= 32 ? FULL : ((1u << hi_b) - 1u)) & (FULL << lo_b);
+    vm = (lane >= c.ys - c.yb && lane < c.ye - c.yb) ? own : 0u;
+    vlo = (lane == 0 && c.ys == 0) ? FULL : 0u;
+    zf = c.zs == 0 ? 1u : 0u;
+    zl = z0 + 32 >= g.W2 ? 0x80000000u : 0u;
+    b0 = lo_b == 0;
+    b31 = hi_b >= 32;
     edge = __any_sync(FULL, yout | (zout != 0));
   }
 };
@@ -284,19 +308,20 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
   {
     uint32_t Cz[8], Cy[8], mzy[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) Cz[i] = bits::shr_fma(C[i], 1);
-    uint32_t gz = bits::gt<8>(C, Cz);
-    if (rg.zlo) gz |= 1u;  // z = -1 never wins as the lower side
+    // z + 1 neighbours; in a last column bit 31's is the virtual collar
+    // (key 255 in every plane: it never wins as the later side)
+    for (int i = 0; i < 8; ++i) Cz[i] = bits::shr1_add(C[i], rg.zl);
+    const uint32_t gz = bits::gt<8>(C, Cz);
     bits::sel<8>(N.mz, gz, C, Cz);
 #pragma unroll
     for (int i = 0; i < 8; ++i) Cy[i] = __shfl_down_sync(FULL, C[i], 1);
-    uint32_t gy = bits::gt<8>(C, Cy);
-    if (rg.y < 0) gy = FULL;  // y = -1 never wins
+    // (lane 31 of a last column reads itself: "y + 1 never wins", the
+    // virtual collar's outcome)
+    const uint32_t gy = bits::gt<8>(C, Cy);
     bits::sel<8>(N.my, gy, C, Cy);
 #pragma unroll
     for (int i = 0; i < 8; ++i) mzy[i] = __shfl_down_sync(FULL, N.mz[i], 1);
-    uint32_t gyz = bits::gt<8>(N.mz, mzy);
-    if (rg.y < 0) gyz = FULL;
+    const uint32_t gyz = bits::gt<8>(N.mz, mzy);
     bits::sel<8>(N.myz, gyz, N.mz, mzy);
     N.gz = gz;
     N.gy = gy;
@@ -310,26 +335,32 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
     uint32_t gxy = bits::gt<8>(P.my, N.my);
     uint32_t g8 = bits::gt<8>(P.myz, N.myz);
     if (KIND == 1 && X - 1 < 0) gxa = gxz = gxy = g8 = FULL;  // x = -1 never wins
-    const uint32_t gxz1 = gxz << 1, g81 = g8 << 1;
-    const uint32_t gxyu = __shfl_up_sync(FULL, gxy, 1);
-    const uint32_t g8u = __shfl_up_sync(FULL, g8, 1);
-    const uint32_t g8u1 = g8u << 1;
+    // z - 1 / y - 1 neighbours' outcomes; across a virtual collar (first
+    // columns: bit 0, lane 0) a block with the collar has the in-image
+    // part's minimum, so its x outcome is that part's
+    const uint32_t gxz1 = bits::shl1_add(gxz, gxa & rg.zf), g81 = bits::shl1_add(g8, gxy & rg.zf);
+    const uint32_t gxyu = bits::bsel(gxa, rg.vlo, __shfl_up_sync(FULL, gxy, 1));
+    const uint32_t g8u = bits::bsel(gxz, rg.vlo, __shfl_up_sync(FULL, g8, 1));
+    const uint32_t g8u1 = bits::shl1_add(g8u, gxyu & rg.zf);
     if constexpr (KIND == 2) {
       // ---- changes of row X-1: each voxel gathers its 26 block wins
-      const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
-      const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
+      // the virtual y = -1 collar never wins: v wins its pair / quads with it
+      const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1) | rg.vlo;
+      const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1) | rg.vlo;
       // the nine in-plane blocks b of each voxel and I_b = "wins b inside
       // the plane": 0 the voxel, 1 / 2 its z- / z+ pair, 3 / 4 its y- / y+
       // pair, 5..8 the yz 4-blocks (y-,z-) (y-,z+) (y+,z-) (y+,z+)
-      const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;
+      // (bit 0 of a first column: the z - 1 pair with the virtual collar is
+      // won by v, and a quad with it reduces to v's y pair)
+      const uint32_t Z0 = ~P.gz, Z1 = bits::shl1_add(P.gz, rg.zf);
       const uint32_t I[9] = {FULL,
                              Z1,
                              Z0,
                              gyu,
                              ~P.gy,
-                             (P.gz & gyzu) << 1,
+                             bits::shl1_add(P.gz & gyzu, gyu & rg.zf),
                              Z0 & gyzu,
-                             (P.gz & ~P.gyz) << 1,
+                             bits::shl1_add(P.gz & ~P.gyz, ~P.gy & rg.zf),
                              Z0 & ~P.gyz};
       // X_b: the next plane's copy of b beats this plane's; Xp_b the same
       // one step earlier (the previous plane against this one)
@@ -353,13 +384,13 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
       bits::transpose_codes(s[0] | ~vm, s[1] | ~vm, s[2] | ~vm, s[3] | ~vm, V);
       if constexpr (CH) {
 #pragma unroll
-        for (int p = 1; p <= 30; ++p) {
+        for (int p = 0; p <= 31; ++p) {
           const int r = p & 7, b = p >> 3;
           const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
                                           (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
           if ((vm >> p) & 1) {
             const long long row = (long long)(X - 1 - g.own0) * g.W1 + rg.y;
-            const long long vox = row * g.W2 + (long long)(zs - 1 + p);
+            const long long vox = row * g.W2 + (long long)(zs + p);
             g.chg[vox] = (int8_t)decode_change(idx >> 8);
           }
         }
@@ -370,15 +401,19 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const int
         // (Predicating the halo lanes' atomics off through grouped asm was
         // measured slower: 161 vs 141 us, the grouping serialises the
         // address computation.)
-#pragma unroll
-        for (int p = 1; p <= 30; ++p) {
+        auto bump = [&](int p) {
           const int r = p & 7, b = p >> 3;
           const uint32_t idx = bits::prmt(P.W[p >> 2], V[r],
                                           (p & 3) | ((4 + b) << 4) | ((0xC + b) << 8) | ((0xC + b) << 12));
           uint32_t addr;
           asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(idx), "r"(g.four), "r"(hist_s));
           asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
-        }
+        };
+#pragma unroll
+        for (int p = 1; p <= 30; ++p) bump(p);
+        // bits 0 / 31 are owned only in a first / last column (warp-uniform)
+        if (rg.b0) bump(0);
+        if (rg.b31) bump(31);
 
       }
     }
@@ -417,7 +452,7 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
       const int X = pc.x0 - 1 + pc.k;  // image plane
       mbar_expect_tx(&myfull[slot], STAGE);
       // TMA needs the axis-2 box origin on a 16-byte boundary
-      tma_load3(myring[slot], &map, ((pc.zs - 1) >> 4) << 4, pc.ys - 1, X - g.plane0, &myfull[slot]);
+      tma_load3(myring[slot], &map, (pc.zb >> 4) << 4, pc.yb, X - g.plane0, &myfull[slot]);
     }
     pc.next(g, nwt);
   };
@@ -433,7 +468,7 @@ __global__ void __launch_bounds__(NW * 32, CTAS_PER_SM)
     Cursor cc;
     cc.start(g, u);
     rg.set(g, cc, lane);
-    const int x0 = cc.x0, zs = cc.zs, len = cc.len;
+    const int x0 = cc.x0, zs = cc.zb, len = cc.len;  // zs: the window's first bit
     // unit planes k = 0 .. len+1 (X = x0-1+k); box b holds planes 2b, 2b+1
     // when PB == 2, one plane per box when PB == 1
     constexpr int S1 = PB == 2 ? 1 : 0;
@@ -517,8 +552,8 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.plane0 = (int)s.plane0;
   g.own0 = (int)s.own0;
   g.P = (int)(s.own1 - s.own0);
-  g.Gy = (g.W1 + 29) / 30;
-  g.Gz = (g.W2 + 29) / 30;
+  g.Gy = col_groups(g.W1);
+  g.Gz = col_groups(g.W2);
   g.ncols = g.Gy * g.Gz;
   g.chg = chg;
   g.four = 4 * HREP;
