@@ -62,6 +62,7 @@ static_assert(hist16::no_wrap(NW * 32, GRP, 7), "3D changes reach -7: the packed
 
 struct Geom {
   int W0, W1, W2, plane0, own0, P, Gy, Gz, ncols, seglen, nunits;
+  int vc;  // virtual-collar column layout (k_u16_3d<true>)
   uint32_t nbins;
   int rr;  // units < resident warps: dealt round-robin over the CTAs (every SM busy)
 };
@@ -99,17 +100,30 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
       : "memory");
 }
 
+// Columns as in k_u8_3d.cu: the first / last column along each in-plane
+// axis owns 31 rows / bits with a virtual collar (ecc_common.cuh cols).
 struct Cursor {
-  int u, k, len, x0, ys, ye, zs, ze;
+  int u, k, len, x0, ys, ye, zs, ze, yb, zb;  // owned [ys, ye) x [zs, ze); window origin (yb, zb)
   __device__ __forceinline__ void set(const Geom& g) {
     const int seg = u / g.ncols, col = u - seg * g.ncols;
     x0 = g.own0 + seg * g.seglen;
     len = min(g.seglen, g.P - seg * g.seglen);
     const int gy = col / g.Gz, gz = col - gy * g.Gz;
-    ys = (int)((long long)gy * g.W1 / g.Gy);
-    ye = (int)((long long)(gy + 1) * g.W1 / g.Gy);
-    zs = (int)((long long)gz * g.W2 / g.Gz);
-    ze = (int)((long long)(gz + 1) * g.W2 / g.Gz);
+    if (g.vc) {
+      ys = cols::start(gy, g.Gy, g.W1);
+      ye = cols::start(gy + 1, g.Gy, g.W1);
+      zs = cols::start(gz, g.Gz, g.W2);
+      ze = cols::start(gz + 1, g.Gz, g.W2);
+      yb = ys > 0 ? ys - 1 : 0;
+      zb = zs > 0 ? zs - 1 : 0;
+    } else {  // every column owns <= 30; the image-edge collar sits in lane 0 / bit 0
+      ys = (int)((long long)gy * g.W1 / g.Gy);
+      ye = (int)((long long)(gy + 1) * g.W1 / g.Gy);
+      zs = (int)((long long)gz * g.W2 / g.Gz);
+      ze = (int)((long long)(gz + 1) * g.W2 / g.Gz);
+      yb = ys - 1;
+      zb = zs - 1;
+    }
   }
   __device__ __forceinline__ void start(const Geom& g, int u0) {
     u = u0;
@@ -139,31 +153,41 @@ struct XCarry {
 struct RunGeom {
   int y, o;
   uint32_t zout, vm;
-  bool yout, zlo, edge;
+  uint32_t vlo, zf, zl;  // virtual-collar substitutions (k_u8_3d.cu RunGeom)
+  bool yout, zlo, edge, b0, b31;
   __device__ __forceinline__ void set(const Geom& g, const Cursor& c, int lane) {
-    y = c.ys - 1 + lane;
-    const int z0 = c.zs - 1;
-    o = z0 - ((z0 >> 3) << 3);  // element offset of the window in the 16-byte aligned box row
+    y = c.yb + lane;
+    const int z0 = c.zb;
+    o = z0 & 7;  // element offset of the window in the 16-byte aligned box row
     yout = (y < 0) | (y >= g.W1);
-    zlo = z0 < 0;
-    const int lo = -z0, hi = g.W2 - z0;
-    uint32_t in = FULL;
-    if (lo > 0) in &= FULL << lo;
-    if (hi < 32) in &= (1u << hi) - 1u;
-    zout = ~in;
-    const int nz = c.ze - c.zs;
-    const uint32_t own = (nz >= 31 ? FULL : ((1u << (nz + 1)) - 1u)) & ~1u;
-    vm = (lane >= 1 && lane <= c.ye - c.ys) ? own : 0u;
+    zlo = z0 < 0;  // the layout without virtual collars: bit 0 is the z = -1 collar
+    const int hi = g.W2 - z0;
+    zout = (hi < 32 ? ~((1u << hi) - 1u) : 0u) | (zlo ? 1u : 0u);
+    const int lo_b = c.zs - z0, hi_b = c.ze - z0;  // owned bits [lo_b, hi_b)
+    const uint32_t own = (hi_b >= 32 ? FULL : ((1u << hi_b) - 1u)) & (FULL << lo_b);
+    vm = (lane >= c.ys - c.yb && lane < c.ye - c.yb) ? own : 0u;
+    vlo = (lane == 0 && c.ys == 0) ? FULL : 0u;
+    zf = c.zs == 0 ? 1u : 0u;
+    zl = z0 + 32 >= g.W2 ? 0x80000000u : 0u;
+    b0 = lo_b == 0;
+    b31 = hi_b >= 32;
     edge = __any_sync(FULL, yout | (zout != 0));
   }
 };
 
+// (x >> 1) + a, a < 2^31 (the z + 1 neighbours; a = the virtual collar bit)
+__device__ __forceinline__ uint32_t shr1_add(uint32_t x, uint32_t a) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(0x80000000u), "r"(a));
+  return d;
+}
+
 // minima of the previous row's blocks, recomputed from its planes
-__device__ __forceinline__ void row_minima(const Row& P, uint32_t (&mz)[16], uint32_t (&my)[16],
-                                           uint32_t (&myz)[16]) {
+__device__ __forceinline__ void row_minima(const Row& P, uint32_t zl, uint32_t (&mz)[16],
+                                           uint32_t (&my)[16], uint32_t (&myz)[16]) {
   uint32_t t[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) t[i] = bits::shr_fma(P.C[i], 1);
+  for (int i = 0; i < 16; ++i) t[i] = shr1_add(P.C[i], zl);
   bits::sel<16>(mz, P.gz, P.C, t);
 #pragma unroll
   for (int i = 0; i < 16; ++i) t[i] = __shfl_down_sync(FULL, P.C[i], 1);
@@ -173,7 +197,7 @@ __device__ __forceinline__ void row_minima(const Row& P, uint32_t (&mz)[16], uin
   bits::sel<16>(myz, P.gyz, mz, t);
 }
 
-template <int KIND, class Issue>
+template <bool VC, int KIND, class Issue>
 __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const RunGeom& rg, int& step,
                                            uint8_t (*myring)[STAGE], uint64_t* myfull,
                                            uint32_t* hwords, uint32_t* pres, int64_t* ghist,
@@ -234,19 +258,19 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
   {
     uint32_t t[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) t[i] = bits::shr_fma(C[i], 1);
+    for (int i = 0; i < 16; ++i) t[i] = shr1_add(C[i], VC ? rg.zl : 0u);
     uint32_t gz = bits::gt<16>(C, t);
-    if (rg.zlo) gz |= 1u;
+    if (!VC && rg.zlo) gz |= 1u;  // z = -1 never wins as the lower side
     bits::sel<16>(Nmz, gz, C, t);
 #pragma unroll
     for (int i = 0; i < 16; ++i) t[i] = __shfl_down_sync(FULL, C[i], 1);
     uint32_t gy = bits::gt<16>(C, t);
-    if (rg.y < 0) gy = FULL;
+    if (!VC && rg.y < 0) gy = FULL;  // y = -1 never wins
     bits::sel<16>(Nmy, gy, C, t);
 #pragma unroll
     for (int i = 0; i < 16; ++i) t[i] = __shfl_down_sync(FULL, Nmz[i], 1);
     uint32_t gyz = bits::gt<16>(Nmz, t);
-    if (rg.y < 0) gyz = FULL;
+    if (!VC && rg.y < 0) gyz = FULL;
     bits::sel<16>(Nmyz, gyz, Nmz, t);
     N.gz = gz;
     N.gy = gy;
@@ -256,25 +280,27 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
     uint32_t gxa, gxz, gxy, g8;
     {
       uint32_t Pmz[16], Pmy[16], Pmyz[16];
-      row_minima(P, Pmz, Pmy, Pmyz);
+      row_minima(P, VC ? rg.zl : 0u, Pmz, Pmy, Pmyz);
       gxa = bits::gt<16>(P.C, N.C);
       gxz = bits::gt<16>(Pmz, Nmz);
       gxy = bits::gt<16>(Pmy, Nmy);
       g8 = bits::gt<16>(Pmyz, Nmyz);
     }
     if (KIND == 1 && X - 1 < 0) gxa = gxz = gxy = g8 = FULL;
-    const uint32_t gxz1 = gxz << 1, g81 = g8 << 1;
-    const uint32_t gxyu = __shfl_up_sync(FULL, gxy, 1);
-    const uint32_t g8u = __shfl_up_sync(FULL, g8, 1);
-    const uint32_t g8u1 = g8u << 1;
+    // across a virtual collar (k_u8_3d.cu): first columns' bit 0 / lane 0
+    const uint32_t zf = VC ? rg.zf : 0u, vlo = VC ? rg.vlo : 0u;
+    const uint32_t gxz1 = (gxz << 1) | (gxa & zf), g81 = (g8 << 1) | (gxy & zf);
+    const uint32_t gxyu = VC ? bits::bsel(gxa, vlo, __shfl_up_sync(FULL, gxy, 1)) : __shfl_up_sync(FULL, gxy, 1);
+    const uint32_t g8u = VC ? bits::bsel(gxz, vlo, __shfl_up_sync(FULL, g8, 1)) : __shfl_up_sync(FULL, g8, 1);
+    const uint32_t g8u1 = (g8u << 1) | (gxyu & zf);
     if constexpr (KIND == 2) {
-      const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1);
-      const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1);
+      const uint32_t gyu = __shfl_up_sync(FULL, P.gy, 1) | vlo;
+      const uint32_t gyzu = __shfl_up_sync(FULL, P.gyz, 1) | vlo;
       // the nine in-plane blocks of each voxel (k_u8_3d.cu): I_b wins b in
       // the plane, X_b / Xp_b the axis-0 comparisons of b, q_b = 2 h_b + l_b
-      const uint32_t Z0 = ~P.gz, Z1 = P.gz << 1;
-      const uint32_t I[9] = {FULL, Z1, Z0, gyu, ~P.gy, (P.gz & gyzu) << 1, Z0 & gyzu,
-                             (P.gz & ~P.gyz) << 1, Z0 & ~P.gyz};
+      const uint32_t Z0 = ~P.gz, Z1 = (P.gz << 1) | zf;
+      const uint32_t I[9] = {FULL, Z1, Z0, gyu, ~P.gy, ((P.gz & gyzu) << 1) | (gyu & zf),
+                             Z0 & gyzu, ((P.gz & ~P.gyz) << 1) | (~P.gy & zf), Z0 & ~P.gyz};
       const uint32_t Xn[9] = {gxa, gxz1, gxz, gxyu, gxy, g8u1, g8u, g81, g8};
       const uint32_t Xp[9] = {xc.gxa, xc.gxz1, xc.gxz, xc.gxyu, xc.gxy,
                               xc.g8u1, xc.g8u, xc.g81, xc.g8};
@@ -303,15 +329,15 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
         atomicAdd(reinterpret_cast<unsigned long long*>(&ghist[key]),
                   static_cast<unsigned long long>(static_cast<long long>(after)));
       };
-      auto voxels = [&](auto with_presence) {
-        // groups of voxels: atomic latencies overlap, one vote per group for
-        // the rare out-of-band fix (hist16.cuh)
+      // one group of NJ voxels p = p0 + j * ps: atomic latencies overlap, one
+      // vote per group for the rare out-of-band fix (hist16.cuh)
+      auto group = [&](auto with_presence, auto nj_c, const int p0, const int ps) {
+        constexpr int NJ = decltype(nj_c)::value;
+        {
+          hist16::Upd u[NJ];
 #pragma unroll
-        for (int g5 = 1; g5 <= 30; g5 += GRP) {
-          hist16::Upd u[GRP];
-#pragma unroll
-          for (int j = 0; j < GRP; ++j) {
-            const int p = g5 + j, r = p & 7, b = p >> 3;
+          for (int j = 0; j < NJ; ++j) {
+            const int p = p0 + j * ps, r = p & 7, b = p >> 3;
             const uint32_t chu =
                 bits::prmt(V[r], 0u, b | ((8 | b) << 4) | ((8 | b) << 8) | ((8 | b) << 12));
             const uint32_t key = bits::prmt(P.W[p >> 1], 0u, (p & 1) ? 0x4432 : 0x4410);
@@ -339,12 +365,19 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
           }
           uint32_t any = 0;
 #pragma unroll
-          for (int j = 0; j < GRP; ++j) any |= hist16::crossed(u[j]);
+          for (int j = 0; j < NJ; ++j) any |= hist16::crossed(u[j]);
           if (__any_sync(FULL, any != 0)) {
 #pragma unroll
-            for (int j = 0; j < GRP; ++j) hist16::fix(hbase, u[j], spill);
+            for (int j = 0; j < NJ; ++j) hist16::fix(hbase, u[j], spill);
           }
         }
+      };
+      auto voxels = [&](auto wp) {
+#pragma unroll
+        for (int g5 = 1; g5 <= 30; g5 += GRP) group(wp, std::integral_constant<int, GRP>{}, g5, 1);
+        // bits 0 / 31 are owned only in a first / last column (warp-uniform)
+        if constexpr (VC)
+          if (rg.b0 | rg.b31) group(wp, std::integral_constant<int, 2>{}, 0, 31);
       };
       uint32_t nset;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nset) : "r"(pbase + PWORDS * 4) : "memory");
@@ -359,6 +392,7 @@ __device__ __forceinline__ void sweep_step(const Geom& g, const int X, const Run
   ++step;
 }
 
+template <bool VC>
 __global__ void __launch_bounds__(NW * 32, 1)
     k_u16_3d(const __grid_constant__ CUtensorMap map, Geom g, int64_t* __restrict__ ghist) {
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -384,7 +418,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     if (lane == 0) {
       const int X = pc.x0 - 1 + pc.k;
       mbar_expect_tx(&myfull[slot], STAGE);
-      tma_load3(myring[slot], &map, ((pc.zs - 1) >> 3) << 3, pc.ys - 1, X - g.plane0,
+      tma_load3(myring[slot], &map, (pc.zb >> 3) << 3, pc.yb, X - g.plane0,
                 &myfull[slot]);
     }
     pc.next(g, nwt);
@@ -399,16 +433,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
     cc.start(g, u);
     rg.set(g, cc, lane);
     const int x0 = cc.x0, len = cc.len;
-    sweep_step<0>(g, x0 - 1, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
-    sweep_step<1>(g, x0, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, A, B, xc, issue);
+    sweep_step<VC, 0>(g, x0 - 1, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
+    sweep_step<VC, 1>(g, x0, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, A, B, xc, issue);
     int X = x0 + 1;
     for (; X + 1 <= x0 + len; X += 2) {
-      sweep_step<2>(g, X, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
-      sweep_step<2>(g, X + 1, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, A, B, xc,
+      sweep_step<VC, 2>(g, X, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
+      sweep_step<VC, 2>(g, X + 1, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, A, B, xc,
                     issue);
     }
     if (X <= x0 + len)
-      sweep_step<2>(g, X, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
+      sweep_step<VC, 2>(g, X, rg, step, myring, myfull, hwords, pres, ghist, pc, lane, B, A, xc, issue);
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < g.nbins; b += NW * 32) {
@@ -550,11 +584,20 @@ cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   g.plane0 = (int)s.plane0;
   g.own0 = (int)s.own0;
   g.P = (int)(s.own1 - s.own0);
-  g.Gy = (g.W1 + 29) / 30;
-  g.Gz = (g.W2 + 29) / 30;
+  // The virtual-collar layout (first / last columns own 31) only where it
+  // saves columns (512: 17 instead of 18 per axis; 1024: 35 either way) --
+  // its substitutions cost registers, so C4's 1024^3 keeps the plain layout.
+  {
+    const int vy = cols::groups(g.W1), vz = cols::groups(g.W2);
+    const int py = (g.W1 + 29) / 30, pz = (g.W2 + 29) / 30;
+    g.vc = (long long)vy * vz < (long long)py * pz;
+    g.Gy = g.vc ? vy : py;
+    g.Gz = g.vc ? vz : pz;
+  }
   g.ncols = g.Gy * g.Gz;
   g.nbins = nbins;
-  smem_optin<k_u16_3d>(SMEM_BYTES);
+  smem_optin<k_u16_3d<false>>(SMEM_BYTES);
+  smem_optin<k_u16_3d<true>>(SMEM_BYTES);
   const long long cap_warps = (long long)sms * NW;
   const long long nseg = best_segments(g.ncols, g.P, cap_warps);
   g.seglen = (int)((g.P + nseg - 1) / nseg);
@@ -566,7 +609,10 @@ cudaError_t launch_u16_3d(const Slab& s, uint32_t nbins, int64_t* ghist, int sms
   g.rr = units < cap_warps;
   const long long grid = g.rr ? std::min<long long>(units, sms)
                               : std::min<long long>((units + NW - 1) / NW, sms);
-  k_u16_3d<<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
+  if (g.vc)
+    k_u16_3d<true><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
+  else
+    k_u16_3d<false><<<(unsigned)grid, NW * 32, SMEM_BYTES, st>>>(map, g, ghist);
   return cudaGetLastError();
 }
 

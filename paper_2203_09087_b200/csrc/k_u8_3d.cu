@@ -151,25 +151,6 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
 // nwt, segment-major) and of the plane step k in [0, len + 2) within it
 // (one halo plane on each side along axis 0); the producer moves a box of
 // PB planes at a time.
-// Column groups along an in-plane axis of width W.  A column's window is 32
-// rows (lanes) / bits; an interior column owns 30 of them (one halo on each
-// side), but the image's first and last columns own 31: the collar beyond
-// the image edge is VIRTUAL (no lane / bit holds it, its comparisons are
-// substituted in sweep_step), so 512 = 31 + 15 x 30 + 31 takes 17 columns
-// instead of 18 (-11 % plane steps at 512^2 per plane).
-__host__ __device__ __forceinline__ int col_groups(int W) {
-  return W <= 32 ? 1 : 2 + (W - 62 + 29) / 30 * (W > 62);
-}
-// First owned index of group k (k = G: W).  W = q G + r; the r groups one
-// voxel larger are taken in the order 0, G-1, 1, 2, ... (only the two edge
-// groups may own 31).
-__host__ __device__ __forceinline__ int col_start(int k, int G, int W) {
-  if (k <= 0) return 0;
-  if (k >= G) return W;
-  const int q = W / G, r = W - q * G;
-  return k * q + (r > 0) + max(0, min(k - 1, r - 2));
-}
-
 struct Cursor {
   int u, k, len, x0, ys, ye, zs, ze, yb, zb;  // owned [ys, ye) x [zs, ze); window origin (yb, zb)
   __device__ __forceinline__ void set(const Geom& g) {
@@ -177,10 +158,10 @@ struct Cursor {
     x0 = g.own0 + seg * g.seglen;
     len = min(g.seglen, g.P - seg * g.seglen);
     const int gy = col / g.Gz, gz = col - gy * g.Gz;
-    ys = col_start(gy, g.Gy, g.W1);
-    ye = col_start(gy + 1, g.Gy, g.W1);
-    zs = col_start(gz, g.Gz, g.W2);
-    ze = col_start(gz + 1, g.Gz, g.W2);
+    ys = cols::start(gy, g.Gy, g.W1);
+    ye = cols::start(gy + 1, g.Gy, g.W1);
+    zs = cols::start(gz, g.Gz, g.W2);
+    ze = cols::start(gz + 1, g.Gz, g.W2);
     yb = ys > 0 ? ys - 1 : 0;  // the first column starts at the image edge (virtual collar)
     zb = zs > 0 ? zs - 1 : 0;
   }
@@ -552,8 +533,8 @@ cudaError_t launch_u8_3d(const Slab& s, int64_t* ghist, int8_t* chg, int sms, cu
   g.plane0 = (int)s.plane0;
   g.own0 = (int)s.own0;
   g.P = (int)(s.own1 - s.own0);
-  g.Gy = col_groups(g.W1);
-  g.Gz = col_groups(g.W2);
+  g.Gy = cols::groups(g.W1);
+  g.Gz = cols::groups(g.W2);
   g.ncols = g.Gy * g.Gz;
   g.chg = chg;
   g.four = 4 * HREP;
