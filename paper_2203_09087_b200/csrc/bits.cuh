@@ -267,4 +267,28 @@ __host__ __device__ __forceinline__ void sum_blocks9(const uint32_t (&h)[9], con
 }
 
 }  // namespace bits
+namespace cols {
+// Column groups of the bit-sliced 3D kernels (k_u8_3d.cu, k_u16_3d.cu)
+// along an in-plane axis of width W.  A column's window is 32
+// rows (lanes) / bits; an interior column owns 30 of them (one halo on each
+// side), but the image's first and last columns own 31: the collar beyond
+// the image edge is VIRTUAL (no lane / bit holds it, its comparisons are
+// substituted in sweep_step), so 512 = 31 + 15 x 30 + 31 takes 17 columns
+// instead of 18 (-11 % plane steps at 512^2 per plane).
+__host__ __device__ __forceinline__ int groups(int W) {
+  return W <= 32 ? 1 : 2 + (W - 62 + 29) / 30 * (W > 62);
+}
+// First owned index of group k (k = G: W).  W = q G + r; the r groups one
+// voxel larger are taken in the order 0, G-1, 1, 2, ... (only the two edge
+// groups may own 31).
+__host__ __device__ __forceinline__ int start(int k, int G, int W) {
+  if (k <= 0) return 0;
+  if (k >= G) return W;
+  const int q = W / G, r = W - q * G;
+  const int m = k - 1 < r - 2 ? k - 1 : r - 2;  // interior groups before k with an extra voxel
+  return k * q + (r > 0) + (m > 0 ? m : 0);
+}
+
+}  // namespace cols
+
 }  // namespace eccb

@@ -121,3 +121,32 @@ static int test_hist16() {
   return 0;
 }
 static int run_hist16 = [] { if (test_hist16()) std::exit(1); return 0; }();  // a failure fails the binary
+
+// Column layout of the bit-sliced 3D kernels (bits.cuh cols): every width
+// is covered exactly, interior columns own <= 30, the two edge columns <= 31
+// (one column: <= 32), and no smaller column count could hold the width.
+static int test_cols() {
+  for (int W = 1; W <= 20000; ++W) {
+    const int G = eccb::cols::groups(W);
+    if (eccb::cols::start(0, G, W) != 0 || eccb::cols::start(G, G, W) != W) {
+      std::printf("cols ends W=%d\n", W);
+      return 1;
+    }
+    for (int k = 0; k < G; ++k) {
+      const int n = eccb::cols::start(k + 1, G, W) - eccb::cols::start(k, G, W);
+      const int cap = G == 1 ? 32 : (k == 0 || k == G - 1) ? 31 : 30;
+      if (n < 1 || n > cap) {
+        std::printf("cols W=%d G=%d k=%d owns %d\n", W, G, k, n);
+        return 1;
+      }
+    }
+    const int cap_less = G - 1 == 1 ? 32 : 30 * (G - 1) + 2;
+    if (G > 1 && W <= cap_less) {
+      std::printf("cols W=%d: %d columns not minimal\n", W, G);
+      return 1;
+    }
+  }
+  std::printf("cols layout ok\n");
+  return 0;
+}
+static int run_cols = [] { if (test_cols()) std::exit(1); return 0; }();

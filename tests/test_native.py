@@ -25,7 +25,7 @@ def _run(args, timeout=600):
 
 def test_bit_sliced_sum_and_code_transpose():
     out = _run([_bin("test_bits")])
-    for name in ("sum_code", "transpose_codes", "sum_blocks9", "hist16 encoding"):
+    for name in ("sum_code", "transpose_codes", "sum_blocks9", "hist16 encoding", "cols layout"):
         assert f"{name} ok" in out, out
 
 
