@@ -101,7 +101,7 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
 }
 
 // Columns as in k_u8_3d.cu: the first / last column along each in-plane
-// axis owns 31 rows / bits with a virtual collar (ecc_common.cuh cols).
+// axis owns 31 rows / bits with a virtual collar (bits.cuh cols).
 struct Cursor {
   int u, k, len, x0, ys, ye, zs, ze, yb, zb;  // owned [ys, ye) x [zs, ze); window origin (yb, zb)
   __device__ __forceinline__ void set(const Geom& g) {
