@@ -1,8 +1,9 @@
 """GPU parity of the bit-sliced 3D u8 kernel (k_u8_3d.cu) against the oracle.
 
 The kernel serves 3D u8 volumes whose axis-2 rows are a multiple of 16
-bytes; it tiles axes 1/2 into 30x30 columns with a 1-voxel halo and splits
-the (column, plane) work evenly over warps, so the cases below target column
+bytes; it tiles axes 1/2 into columns of 30 (31 at the image edges: virtual
+collar, tests/test_gpu_columns.py) with a 1-voxel halo and splits the
+(column, plane) work evenly over warps, so the cases below target column
 edges, uneven splits, tiny dims, slabs, ties around 255 (the collar value)
 and constant / plateau inputs.  Bit-exact.
 """
