@@ -10,8 +10,10 @@
 //
 // Mapping.  A warp owns a "column": 32 rows along axis 1 (one per lane) x
 // 32 voxels along axis 2 (one per bit of a bit plane) and sweeps a segment
-// of axis 0.  Lane 0 / 31 and bit 0 / 31 are halo, so a column yields up to
-// 30 x 30 voxels per plane.  Work units are (segment, column) pairs in
+// of axis 0.  Lane 0 / 31 and bit 0 / 31 are halo, so an interior column
+// yields up to 30 x 30 voxels per plane; the first / last column along an
+// axis owns 31 there, its collar lane / bit being virtual (bits.cuh cols,
+// the substitutions in sweep_step).  Work units are (segment, column) pairs in
 // segment-major order: warps that run at the same time hold neighbouring
 // columns at the same axis-0 position, so the halo rows/bytes a column
 // shares with its neighbours are read from DRAM once and hit in L2 after.
