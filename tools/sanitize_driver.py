@@ -39,6 +39,13 @@ for shape in [(40, 1000), (3, 5), (17, 961)]:
     check(f"u16 2D {shape}", ctx.vcec(img16), img16)
 img16 = rng.integers(0, 65536, (12, 40, 48)).astype(np.uint16)
 check("u16 3D", ctx.vcec(img16), img16)
+# column-layout boundaries (first / last columns with a virtual collar, bits.cuh cols)
+for shape in [(4, 62, 64), (3, 93, 96), (2, 512, 512), (3, 32, 32)]:
+    img = rng.integers(250, 256, shape).astype(np.uint8)
+    check(f"u8 3D columns {shape}", ctx.vcec(img), img)
+for shape in [(4, 62, 64), (3, 93, 40), (2, 512, 512)]:
+    img16 = rng.integers(0, 65536, shape).astype(np.uint16)
+    check(f"u16 3D columns {shape}", ctx.vcec(img16), img16)
 q = (rng.integers(0, 65536, (10, 33, 40)) * 2.0 ** -16).astype(np.float32)
 check("f32 affine 3D", ctx.vcec(q, binmap=eb.quantised_binmap(65536)), q)
 q2 = (rng.integers(0, 65536, (50, 70)) * 2.0 ** -16).astype(np.float32)
